@@ -1,0 +1,557 @@
+"""TEST INFRASTRUCTURE ONLY -- CPU parity oracle for the Q-less tall-skinny QR hot path.
+
+Two checkers live here, both loaded through ctypes:
+
+* ``oracle.port``  -- ``oracle_c.c``, a plain-C restatement of the reference algorithms
+  (each function cites the reference file:line it follows).  Always buildable.
+* ``oracle.ref``   -- ``oracle/_ref/libskinnyqr_ref.so``: the UNMODIFIED reference sources
+  compiled where they lie under /root/reference/proj plus ``ref_shim.cpp`` (a C ABI around
+  them).  Built in the dev container by ``make -C oracle ref``; the prebuilt ``.so`` travels
+  to the GPU box.  ``oracle.ref`` is ``None`` when it is absent.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline / ``--impl
+reference`` legs may import this package.  The product never does.
+
+All matrices are numpy float64 arrays in Fortran (column-major) order, matching the reference's
+``data[j*rows + i]`` layout (types.hpp:79,94).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+PORT_SO = HERE / "_build" / "liboracle.so"
+REF_SO = HERE / "_ref" / "libskinnyqr_ref.so"
+
+I64 = C.c_longlong
+U64 = C.c_ulonglong
+DP = C.POINTER(C.c_double)
+IP = C.POINTER(I64)
+
+STATUS_NAMES = {
+    0: "ok",
+    -1: "DimensionError",
+    -2: "ArgumentError",
+    -3: "BreakdownError",
+    -4: "SingularFactorError",
+    -5: "ZeroMatrixError",
+    -6: "RankDeficiencyError",
+    -7: "Error",
+}
+
+
+class OracleError(Exception):
+    """Mirrors a reference exception: ``kind`` is the reference class name."""
+
+    def __init__(self, status: int, index: int = -1, where: str = ""):
+        self.status = status
+        self.kind = STATUS_NAMES.get(status, f"status {status}")
+        self.index = index
+        super().__init__(f"{where}: {self.kind}" + (f" (index {index})" if index >= 0 else ""))
+
+
+def build(ref: bool = True) -> None:
+    """Compile the C port (always) and the reference library (only if its sources exist)."""
+    targets = ["oracle"] + (["ref"] if ref else [])
+    subprocess.run(["make", "-s", "-C", str(HERE)] + targets, check=True)
+
+
+def fmat(a, dtype=np.float64) -> np.ndarray:
+    return np.asfortranarray(np.asarray(a, dtype=dtype))
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(DP)
+
+
+def _check(st: int, where: str, idx=None):
+    if st != 0:
+        raise OracleError(st, int(idx.value) if idx is not None else -1, where)
+
+
+def _square(n):
+    return np.zeros((n, n), dtype=np.float64, order="F")
+
+
+class _Port:
+    """ctypes view of oracle_c.c."""
+
+    def __init__(self):
+        if not PORT_SO.exists():
+            build(ref=False)
+        L = C.CDLL(str(PORT_SO))
+        self.L = L
+        L.orc_mix64.restype = U64
+        L.orc_mix64.argtypes = [U64, U64]
+        L.orc_uniform01.restype = C.c_double
+        L.orc_uniform01.argtypes = [U64, U64]
+        L.orc_trsm_diag_tolerance.restype = C.c_double
+        for name in ("orc_rows_per_block", "orc_block_begin", "orc_block_end",
+                     "orc_default_tsqr_panel_rows", "orc_default_gram_panel_rows"):
+            getattr(L, name).restype = I64
+            getattr(L, name).argtypes = None
+        self.threads = os.cpu_count() or 1
+
+    # -- stream / generator
+    def mix64(self, seed, index):
+        return int(self.L.orc_mix64(U64(seed), U64(index)))
+
+    def uniform01(self, seed, index):
+        return float(self.L.orc_uniform01(U64(seed), U64(index)))
+
+    def generate(self, m, n, kappa, seed, linear=False):
+        x = np.zeros((m, n), order="F")
+        _check(self.L.orc_generate(I64(m), I64(n), C.c_double(kappa), C.c_int(int(linear)),
+                                   U64(seed), _p(x)), "generate")
+        return x
+
+    # -- plans
+    def default_tsqr_plan(self, m, n):
+        b = int(self.L.orc_default_tsqr_panel_rows(I64(n)))
+        if b < 0:
+            raise OracleError(b, -1, "default_tsqr_plan")
+        return self.threads, b
+
+    def default_gram_plan(self, m, n):
+        return self.threads, int(self.L.orc_default_gram_panel_rows(I64(n)))
+
+    def block_range(self, m, k, b, blk):
+        return (int(self.L.orc_block_begin(I64(m), I64(k), I64(b), I64(blk))),
+                int(self.L.orc_block_end(I64(m), I64(k), I64(b), I64(blk))))
+
+    def _plan(self, m, n, k, b, tsqr):
+        dk, db = self.default_tsqr_plan(m, n) if tsqr else self.default_gram_plan(m, n)
+        return (k or dk), (b or db)
+
+    # -- TSQR
+    def factor_trapezoidal(self, w, b):
+        w = fmat(w)
+        p, n = w.shape
+        out = np.zeros((b + n, n), order="F")
+        _check(self.L.orc_factor_trapezoidal(_p(w), I64(p), I64(n), I64(b), _p(out)),
+               "factor_trapezoidal")
+        return out
+
+    def block_qless_qr(self, x, b):
+        x = fmat(x)
+        m, n = x.shape
+        r = _square(n)
+        _check(self.L.orc_block_qless_qr(_p(x), I64(m), I64(n), I64(b), _p(r)), "block_qless_qr")
+        return r
+
+    def tsqr_stage1(self, x, k=0, b=0):
+        x = fmat(x)
+        m, n = x.shape
+        k, b = self._plan(m, n, k, b, True)
+        y = np.zeros((k * n, n), order="F")
+        _check(self.L.orc_tsqr_stage1(_p(x), I64(m), I64(n), I64(k), I64(b), _p(y)), "tsqr_stage1")
+        return y
+
+    def tsqr_qless(self, x, k=0, b=0):
+        x = fmat(x)
+        m, n = x.shape
+        if n > 64:
+            raise OracleError(-2, -1, "tsqr_qless")
+        k, b = self._plan(m, max(n, 1), k, b, True)
+        r = _square(n)
+        _check(self.L.orc_tsqr_qless(_p(x), I64(m), I64(n), I64(k), I64(b), _p(r)), "tsqr_qless")
+        return r
+
+    def reference_hhqr(self, x):
+        x = fmat(x)
+        m, n = x.shape
+        r = _square(n)
+        _check(self.L.orc_reference_hhqr(_p(x), I64(m), I64(n), _p(r)), "reference_hhqr")
+        return r
+
+    def hhqr_small(self, a):
+        a = fmat(a)
+        m, n = a.shape
+        r = _square(n)
+        _check(self.L.orc_hhqr_small(_p(a), I64(m), I64(n), _p(r)), "hhqr_small")
+        return r
+
+    # -- Gram
+    def tsmttsm(self, x, k=0, b=0):
+        x = fmat(x)
+        m, n = x.shape
+        k, b = self._plan(m, n, k, b, False)
+        c = _square(n)
+        _check(self.L.orc_tsmttsm(_p(x), I64(m), I64(n), I64(k), I64(b), _p(c)), "tsmttsm")
+        return c
+
+    def tsmRttsmR(self, x, r, k=0, b=0):
+        x, r = fmat(x), fmat(r)
+        m, n = x.shape
+        if r.shape != (n, n):
+            raise OracleError(-1, -1, "tsmRttsmR")
+        k, b = self._plan(m, n, k, b, False)
+        c, idx = _square(n), I64(-1)
+        _check(self.L.orc_tsmRttsmR(_p(x), I64(m), I64(n), _p(r), I64(k), I64(b), _p(c),
+                                    C.byref(idx)), "tsmRttsmR", idx)
+        return c
+
+    def tsmmttsmm(self, x, bm, k=0, b=0):
+        x, bm = fmat(x), fmat(bm)
+        m, n = x.shape
+        if bm.shape != (n, n):
+            raise OracleError(-1, -1, "tsmmttsmm")
+        k, b = self._plan(m, n, k, b, False)
+        c = _square(n)
+        _check(self.L.orc_tsmmttsmm(_p(x), I64(m), I64(n), _p(bm), I64(k), I64(b), _p(c)),
+               "tsmmttsmm")
+        return c
+
+    # -- n x n
+    def cholesky(self, c):
+        c = fmat(c)
+        n = c.shape[0]
+        r, idx = _square(n), I64(-1)
+        _check(self.L.orc_cholesky(_p(c), I64(n), _p(r), C.byref(idx)), "cholesky", idx)
+        return r
+
+    def eigh_small(self, c):
+        c = fmat(c)
+        n = c.shape[0]
+        vals, vecs = np.zeros(n), _square(n)
+        _check(self.L.orc_eigh_small(_p(c), I64(n), _p(vals), _p(vecs)), "eigh_small")
+        return vals, vecs
+
+    def triangular_multiply(self, a, b):
+        a, b = fmat(a), fmat(b)
+        n = a.shape[0]
+        out = _square(n)
+        self.L.orc_triangular_multiply(_p(a), _p(b), I64(n), _p(out))
+        return out
+
+    # -- drivers
+    def cholqr2(self, x, k=0, b=0):
+        x = fmat(x)
+        m, n = x.shape
+        k, b = self._plan(m, n, k, b, False)
+        r, idx = _square(n), I64(-1)
+        _check(self.L.orc_cholqr2(_p(x), I64(m), I64(n), I64(k), I64(b), _p(r), C.byref(idx)),
+               "cholqr2", idx)
+        return r
+
+    def svqb_pass(self, c):
+        c = fmat(c)
+        n = c.shape[0]
+        bm, z, sg, rank = _square(n), _square(n), np.zeros(n), I64(0)
+        _check(self.L.orc_svqb_pass(_p(c), I64(n), _p(bm), _p(z), _p(sg), C.byref(rank)),
+               "svqb_pass")
+        return bm, z, sg, int(rank.value)
+
+    def svqb2(self, x, k=0, b=0):
+        x = fmat(x)
+        m, n = x.shape
+        k, b = self._plan(m, n, k, b, False)
+        tr, z, sg, rank = _square(n), _square(n), np.zeros(n), I64(0)
+        _check(self.L.orc_svqb2(_p(x), I64(m), I64(n), I64(k), I64(b), _p(tr), _p(z), _p(sg),
+                                C.byref(rank)), "svqb2")
+        return tr, z, sg, int(rank.value)
+
+    def reconstruct_q(self, x, r):
+        x, r = fmat(x), fmat(r)
+        m, n = x.shape
+        q, idx = np.zeros((m, n), order="F"), I64(-1)
+        _check(self.L.orc_reconstruct_q(_p(x), I64(m), I64(n), _p(r), _p(q), C.byref(idx)),
+               "reconstruct_q", idx)
+        return q
+
+    def solve_lstsq(self, a, rhs, method="tsqr"):
+        a = fmat(a)
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        m, n = a.shape
+        if rhs.shape != (m,):
+            raise OracleError(-1, -1, "solve_lstsq")
+        meth = {"tsqr": 0, "cholqr2": 1, "svqb2": 2}[method]
+        x, res, idx = np.zeros(n), C.c_double(0.0), I64(-1)
+        _check(self.L.orc_solve_lstsq(_p(a), I64(m), I64(n), _p(rhs), C.c_int(meth),
+                                      I64(self.threads), _p(x), C.byref(res), C.byref(idx)),
+               "solve_lstsq", idx)
+        return x, float(res.value)
+
+
+class _Ref:
+    """ctypes view of the compiled, unmodified reference (oracle/_ref)."""
+
+    METHODS = {"tsqr": 0, "cholqr2": 1, "svqb2": 2, "tsqr_novalidate": 3, "hhqr": 4, "tsmttsm": 5}
+
+    def __init__(self):
+        L = C.CDLL(str(REF_SO))
+        self.L = L
+        L.ref_last_message.restype = C.c_char_p
+        L.ref_kernel_table_name.restype = C.c_char_p
+        L.ref_max_threads.restype = I64
+        L.ref_mix64.restype = U64
+        L.ref_mix64.argtypes = [U64, U64]
+        L.ref_uniform01.restype = C.c_double
+        L.ref_uniform01.argtypes = [U64, U64]
+        L.ref_matrix_create.restype = C.c_void_p
+        L.ref_matrix_create_uninit.restype = C.c_void_p
+        L.ref_matrix_data.restype = DP
+        L.ref_matrix_data.argtypes = [C.c_void_p]
+        L.ref_matrix_destroy.argtypes = [C.c_void_p]
+
+    @property
+    def threads(self):
+        return int(self.L.ref_max_threads())
+
+    def set_threads(self, n):
+        self.L.ref_set_max_threads(I64(n))
+
+    def kernel_table(self):
+        return self.L.ref_kernel_table_name().decode()
+
+    def select_kernel_table(self, name):
+        return self.L.ref_select_kernel_table(C.c_int(0 if name == "scalar" else 1)) == 0
+
+    def counters_reset(self):
+        self.L.ref_counters_reset()
+
+    def counters(self):
+        out = (U64 * 4)()
+        self.L.ref_counters_read(out)
+        return dict(zip(("large_reads", "large_writes", "flops", "flops_actual"), map(int, out)))
+
+    def mix64(self, seed, index):
+        return int(self.L.ref_mix64(U64(seed), U64(index)))
+
+    def uniform01(self, seed, index):
+        return float(self.L.ref_uniform01(U64(seed), U64(index)))
+
+    def generate(self, m, n, kappa, seed, linear=False):
+        x = np.zeros((m, n), order="F")
+        _check(self.L.ref_generate(I64(m), I64(n), C.c_double(kappa), C.c_int(int(linear)),
+                                   U64(seed), _p(x)), "generate")
+        return x
+
+    def default_tsqr_plan(self, m, n):
+        k, b = I64(0), I64(0)
+        _check(self.L.ref_default_tsqr_plan(I64(m), I64(n), C.byref(k), C.byref(b)),
+               "default_tsqr_plan")
+        return int(k.value), int(b.value)
+
+    def default_gram_plan(self, m, n):
+        k, b = I64(0), I64(0)
+        _check(self.L.ref_default_gram_plan(I64(m), I64(n), C.byref(k), C.byref(b)),
+               "default_gram_plan")
+        return int(k.value), int(b.value)
+
+    def block_range(self, m, k, b, blk):
+        lo, hi = I64(0), I64(0)
+        self.L.ref_plan_block_range(I64(m), I64(k), I64(b), I64(blk), C.byref(lo), C.byref(hi))
+        return int(lo.value), int(hi.value)
+
+    def factor_trapezoidal(self, w, b):
+        w = fmat(w)
+        p, n = w.shape
+        out = np.zeros((b + n, n), order="F")
+        _check(self.L.ref_factor_trapezoidal(_p(w), I64(p), I64(n), I64(b), _p(out)),
+               "factor_trapezoidal")
+        return out
+
+    def block_qless_qr(self, x, b):
+        x = fmat(x)
+        m, n = x.shape
+        r = _square(n)
+        _check(self.L.ref_block_qless_qr(_p(x), I64(m), I64(n), I64(b), _p(r)), "block_qless_qr")
+        return r
+
+    def tsqr_stage1(self, x, k=0, b=0):
+        x = fmat(x)
+        m, n = x.shape
+        kk = k or self.threads
+        y = np.zeros((kk * n, n), order="F")
+        _check(self.L.ref_tsqr_stage1(_p(x), I64(m), I64(n), I64(k), I64(b), _p(y)), "tsqr_stage1")
+        return y
+
+    def tsqr_qless(self, x, k=0, b=0):
+        x = fmat(x)
+        m, n = x.shape
+        r = _square(n)
+        _check(self.L.ref_tsqr_qless(_p(x), I64(m), I64(n), I64(k), I64(b), _p(r)), "tsqr_qless")
+        return r
+
+    def reference_hhqr(self, x):
+        x = fmat(x)
+        m, n = x.shape
+        r = _square(n)
+        _check(self.L.ref_reference_hhqr(_p(x), I64(m), I64(n), _p(r)), "reference_hhqr")
+        return r
+
+    def hhqr_small(self, a):
+        a = fmat(a)
+        m, n = a.shape
+        r = _square(n)
+        _check(self.L.ref_hhqr_small(_p(a), I64(m), I64(n), _p(r)), "hhqr_small")
+        return r
+
+    def tsmttsm(self, x, k=0, b=0, deterministic=True):
+        x = fmat(x)
+        m, n = x.shape
+        c = _square(n)
+        _check(self.L.ref_tsmttsm(_p(x), I64(m), I64(n), I64(k), I64(b),
+                                  C.c_int(int(deterministic)), _p(c)), "tsmttsm")
+        return c
+
+    def tsmRttsmR(self, x, r, k=0, b=0):
+        x, r = fmat(x), fmat(r)
+        m, n = x.shape
+        if r.shape[0] != n:
+            raise OracleError(-1, -1, "tsmRttsmR")
+        c, idx = _square(n), I64(-1)
+        _check(self.L.ref_tsmRttsmR(_p(x), I64(m), I64(n), _p(r), I64(k), I64(b), _p(c),
+                                    C.byref(idx)), "tsmRttsmR", idx)
+        return c
+
+    def tsmmttsmm(self, x, bm, k=0, b=0):
+        x, bm = fmat(x), fmat(bm)
+        m, n = x.shape
+        if bm.shape != (n, n):
+            raise OracleError(-1, -1, "tsmmttsmm")
+        c = _square(n)
+        _check(self.L.ref_tsmmttsmm(_p(x), I64(m), I64(n), _p(bm), I64(k), I64(b), _p(c)),
+               "tsmmttsmm")
+        return c
+
+    def cholesky(self, c):
+        c = fmat(c)
+        n = c.shape[0]
+        r, idx = _square(n), I64(-1)
+        _check(self.L.ref_cholesky(_p(c), I64(n), _p(r), C.byref(idx)), "cholesky", idx)
+        return r
+
+    def eigh_small(self, c):
+        c = fmat(c)
+        n = c.shape[0]
+        vals, vecs = np.zeros(n), _square(n)
+        _check(self.L.ref_eigh_small(_p(c), I64(n), _p(vals), _p(vecs)), "eigh_small")
+        return vals, vecs
+
+    def triangular_multiply(self, a, b):
+        a, b = fmat(a), fmat(b)
+        n = a.shape[0]
+        out = _square(n)
+        _check(self.L.ref_triangular_multiply(_p(a), _p(b), I64(n), _p(out)), "triangular_multiply")
+        return out
+
+    def cholqr2(self, x, k=0, b=0):
+        x = fmat(x)
+        m, n = x.shape
+        r, idx = _square(n), I64(-1)
+        _check(self.L.ref_cholqr2(_p(x), I64(m), I64(n), I64(k), I64(b), _p(r), C.byref(idx)),
+               "cholqr2", idx)
+        return r
+
+    def svqb_pass(self, c):
+        c = fmat(c)
+        n = c.shape[0]
+        bm, z, sg, rank = _square(n), _square(n), np.zeros(n), I64(0)
+        _check(self.L.ref_svqb_pass(_p(c), I64(n), _p(bm), _p(z), _p(sg), C.byref(rank)),
+               "svqb_pass")
+        return bm, z, sg, int(rank.value)
+
+    def svqb2(self, x, k=0, b=0):
+        x = fmat(x)
+        m, n = x.shape
+        tr, z, sg, rank = _square(n), _square(n), np.zeros(n), I64(0)
+        _check(self.L.ref_svqb2(_p(x), I64(m), I64(n), I64(k), I64(b), _p(tr), _p(z), _p(sg),
+                                C.byref(rank)), "svqb2")
+        return tr, z, sg, int(rank.value)
+
+    def reconstruct_q(self, x, r):
+        x, r = fmat(x), fmat(r)
+        m, n = x.shape
+        q, idx = np.zeros((m, n), order="F"), I64(-1)
+        _check(self.L.ref_reconstruct_q(_p(x), I64(m), I64(n), _p(r), _p(q), C.byref(idx)),
+               "reconstruct_q", idx)
+        return q
+
+    def solve_lstsq(self, a, rhs, method="tsqr"):
+        a = fmat(a)
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        m, n = a.shape
+        if rhs.shape != (m,):
+            raise OracleError(-1, -1, "solve_lstsq")
+        meth = {"tsqr": 0, "cholqr2": 1, "svqb2": 2}[method]
+        x, res, idx = np.zeros(n), C.c_double(0.0), I64(-1)
+        _check(self.L.ref_solve_lstsq(_p(a), I64(m), I64(n), _p(rhs), C.c_int(meth), _p(x),
+                                      C.byref(res), C.byref(idx)), "solve_lstsq", idx)
+        return x, float(res.value)
+
+    # -- timed handles for the CPU baseline (bench.py)
+    def matrix_handle(self, m, n):
+        """Allocate a reference DenseMatrix and return (handle, numpy view of its storage)."""
+        h = self.L.ref_matrix_create_uninit(I64(m), I64(n))
+        ptr = self.L.ref_matrix_data(C.c_void_p(h))
+        view = np.ctypeslib.as_array(ptr, shape=(n, m)).T  # F-order m x n view
+        return h, view
+
+    def matrix_destroy(self, h):
+        self.L.ref_matrix_destroy(C.c_void_p(h))
+
+    def timed(self, h, method, n, k=0, b=0, want_result=False):
+        out = _square(n) if want_result else None
+        secs = C.c_double(0.0)
+        st = self.L.ref_timed_factor(C.c_void_p(h), C.c_int(self.METHODS[method]), I64(k), I64(b),
+                                     _p(out) if want_result else None, C.byref(secs))
+        _check(st, f"timed[{method}]")
+        return float(secs.value), out
+
+
+def _load_port():
+    return _Port()
+
+
+def _load_ref():
+    if not REF_SO.exists():
+        if Path("/root/reference/proj/src").is_dir():
+            build(ref=True)
+        if not REF_SO.exists():
+            return None
+    try:
+        return _Ref()
+    except OSError:
+        return None
+
+
+port = _load_port()
+ref = _load_ref()
+
+
+def gaussian(m: int, n: int, seed: int = 1234) -> np.ndarray:
+    """Synthetic Gaussian input as defined in SURVEY.md 8(d): Box-Muller over the reference's
+    uniform01 stream, element e = j*m + i uses stream positions 2e, 2e+1.  (The reference ships
+    no Gaussian generator; this is the harness definition, vectorised with numpy.)"""
+    e = np.arange(m * n, dtype=np.uint64)
+
+    def mix(idx):
+        with np.errstate(over="ignore"):
+            z = np.uint64(seed) + (idx + np.uint64(1)) * np.uint64(0x9E3779B97F4A7C15)
+            z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+            z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+            return z ^ (z >> np.uint64(31))
+
+    u1 = (mix(e * np.uint64(2)) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    u2 = (mix(e * np.uint64(2) + np.uint64(1)) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    g = np.sqrt(-2.0 * np.log(np.maximum(u1, 2.0 ** -53))) * np.cos(2.0 * np.pi * u2)
+    return np.asfortranarray(g.reshape((n, m)).T)
+
+
+def uniform_pm1(m: int, n: int, seed: int) -> np.ndarray:
+    """Bit-reproducible test input: 2*uniform01(seed, j*m+i) - 1 (exact arithmetic only)."""
+    e = np.arange(m * n, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed) + (e + np.uint64(1)) * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    u = (z >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    return np.asfortranarray((2.0 * u - 1.0).reshape((n, m)).T)
