@@ -1,0 +1,132 @@
+// Shared device helpers for the sm_100a kernels: mbarrier + bulk-copy (TMA engine) staging,
+// warp-private panel stages, FP64 scalar helpers and the device status word.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "skinnyqr_b200.h"
+
+namespace sqb {
+
+constexpr int kWarp = 32;
+
+// ---------------------------------------------------------------------------------------
+// Device status word (one per context, lives in device memory, mirrored to the host on sync).
+// word[0] = first error code raised (0 = none), word[1] = index attached to it,
+// word[2] = non-finite-input flag (raised by the streaming kernels' fused validation).
+// ---------------------------------------------------------------------------------------
+struct StatusWord {
+  int code;
+  int index;
+  int nonfinite;
+  int reserved;
+};
+
+__device__ __forceinline__ void raise_status(StatusWord* st, int code, int index) {
+  if (atomicCAS(&st->code, 0, code) == 0) st->index = index;
+}
+
+// ---------------------------------------------------------------------------------------
+// mbarrier / bulk async copy (cp.async.bulk = the TMA engine's 1-D path; SASS: UBLKCP).
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_addr(bar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  }
+}
+
+// Generic-proxy reads of a stage must be ordered before the async proxy overwrites it.
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// One contiguous global -> shared bulk copy; completion is signalled on `bar` as transaction
+// bytes.  dst, src and bytes must all be multiples of 16.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+// ---------------------------------------------------------------------------------------
+// FP64 helpers
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ double shfl_xor_f64(double v, int mask) {
+  return __shfl_xor_sync(0xffffffffu, v, mask);
+}
+__device__ __forceinline__ double shfl_idx_f64(double v, int src) {
+  return __shfl_sync(0xffffffffu, v, src);
+}
+
+// Exponent-field test: true when x is Inf or NaN.  Integer pipe only (keeps the FP64 pipe free).
+__device__ __forceinline__ uint32_t nonfinite_bits(double x) {
+  return static_cast<uint32_t>(__double2hiint(x)) & 0x7fffffffu;
+}
+constexpr uint32_t kNonFiniteHi = 0x7ff00000u;
+
+// sqrt(a) for a >= 0 built on the reciprocal-square-root unit plus one residual correction
+// (result within 1 ulp of the correctly rounded root); returns 0 for a == 0.
+__device__ __forceinline__ double sqrt_pos(double a) {
+  const double y = rsqrt(a);
+  double r = a * y;
+  const double e = fma(-r, r, a);
+  r = fma(e, 0.5 * y, r);
+  return a > 0.0 ? r : (a == 0.0 ? 0.0 : a * y);  // a*y propagates NaN/Inf
+}
+
+// Householder reflector scalars for the pencil [pivot; tail], sigma = |tail|^2, in the
+// un-normalised form  H = I - gamma * u u^T,  u = [u0; tail],  u0 = pivot - beta,
+// gamma = 1 / (beta * (beta - pivot)).  Same sign convention as the reference's
+// make_reflector (tsqr.cpp:51-71): beta = -norm when pivot > 0 else +norm; sigma == 0 gives the
+// identity (gamma = 0, beta = pivot) so a zero column keeps an exact zero diagonal.
+struct Reflector {
+  double beta, u0, gamma;
+};
+__device__ __forceinline__ Reflector make_reflector(double pivot, double sigma) {
+  Reflector h;
+  const double norm = sqrt_pos(fma(pivot, pivot, sigma));
+  const double beta = pivot > 0.0 ? -norm : norm;
+  const double u0 = pivot - beta;
+  const double den = beta * (-u0);
+  const bool live = sigma != 0.0;
+  h.beta = live ? beta : pivot;
+  h.u0 = live ? u0 : 0.0;
+  h.gamma = live ? __drcp_rn(den) : 0.0;
+  return h;
+}
+
+// Packed upper-triangular storage: column j holds rows 0..j at offset j(j+1)/2.
+__host__ __device__ __forceinline__ int tri_index(int i, int j) { return j * (j + 1) / 2 + i; }
+__host__ __device__ __forceinline__ int tri_size(int n) { return n * (n + 1) / 2; }
+
+}  // namespace sqb

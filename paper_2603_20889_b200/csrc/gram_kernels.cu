@@ -1,0 +1,338 @@
+// Fused Gram streaming kernels (sm_100a): one pass over X, no m x n intermediate ever leaves the SM.
+//
+//   OP_PLAIN     C = X^T X                      reference tsmttsm    (src/gram.cpp:113-121)
+//   OP_SOLVE     C = (X R^-1)^T (X R^-1)        reference tsmRttsmR  (src/gram.cpp:123-140)
+//   OP_MULTIPLY  C = (X B)^T (X B)              reference tsmmttsmm  (src/gram.cpp:142-151)
+//
+// Structure (reference blocked_gram, src/gram.cpp:23-94): one CTA per plan block, private
+// upper-triangle partial per block, partials summed in ascending block order by
+// gram_reduce_kernel (deterministic mode, gram.cpp:81-92), then mirrored.
+//
+// B200 design: every warp streams its own panels through TMA-fed private stages.  The rank-P
+// update runs on the FP64 tensor pipe: lane (g,q) of a warp holds X[row(q), 8b+g], which is at
+// the same time the A fragment (8 columns x 4 rows, transposed) and the B fragment (4 rows x 8
+// columns) of mma.m8n8k4.f64 - so  C[8b.., 8b'..] += mma(w[b], w[b'])  needs no data movement.
+//   * OP_SOLVE applies R^-1 to the register panel by column-oriented substitution, the order the
+//     reference's trsm_right_upper uses (src/kernels_scalar.cpp:19-32), broadcasting each finished
+//     column through a P-double buffer; the panel never leaves registers before the Gram MMAs.
+//   * OP_MULTIPLY forms (X B) for 8 rows at a time with DMMAs whose accumulator layout is exactly
+//     the Gram fragment layout, then feeds those accumulators straight into the Gram MMAs.
+#include "kernels.h"
+
+namespace sqb {
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int NB, int OP>
+struct GramCfg {
+  static constexpr int NPAD = 8 * NB;
+  static constexpr int NW = NB >= 8 ? 6 : 8;
+  static constexpr int NS = OP == OP_SOLVE ? 1 : 2;
+  static constexpr int RL = WarpCfg<NB>::RL;  // OP_SOLVE: register panel, same shape as TSQR
+  // streaming panel heights: P == 8 (mod 16) keeps the plain fragment pattern unpadded, P == 0
+  // (mod 16) costs the transposed pattern only 4 pad rows
+  static constexpr int kPlainP[8] = {120, 72, 40, 40, 24, 24, 24, 24};
+  static constexpr int kMultP[8] = {112, 64, 48, 32, 32, 16, 16, 16};
+  static constexpr int P =
+      OP == OP_SOLVE ? 4 * RL : (OP == OP_PLAIN ? kPlainP[NB - 1] : kMultP[NB - 1]);
+  static constexpr int PP = stage_pitch(P, OP == OP_MULTIPLY ? 4 : 8);
+  static constexpr int kStageDoubles = NPAD * PP;
+  static constexpr int kVbuf = OP == OP_SOLVE ? P : 0;
+  static constexpr int kWarpDoubles = NS * kStageDoubles + kVbuf + 2 * NS;  // + mbarrier slots
+  static constexpr int FP = NPAD + 4;  // factor pitch: conflict-free A-fragment reads
+  static constexpr int kFacDoubles = OP == OP_PLAIN ? 0 : NPAD * FP + NPAD;
+  static constexpr int kSumDoubles = NPAD * NPAD;
+  static constexpr size_t kSmemBytes =
+      sizeof(double) * (static_cast<size_t>(kWarpDoubles) * NW + kFacDoubles + kSumDoubles);
+  static constexpr int NPAIR = NB * (NB + 1) / 2;
+  static_assert(P >= 8 && P % 8 == 0, "panel rows");
+  static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
+};
+
+template <int NB, int OP>
+__global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
+    gram_mma_kernel(const GramParams prm) {
+  using Cfg = GramCfg<NB, OP>;
+  constexpr int P = Cfg::P, PP = Cfg::PP, NW = Cfg::NW, NS = Cfg::NS, NPAD = Cfg::NPAD;
+  constexpr int FP = Cfg::FP, NPAIR = Cfg::NPAIR;
+  extern __shared__ __align__(128) double smem[];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int n = prm.n;
+
+  double* my = smem + static_cast<size_t>(warp) * Cfg::kWarpDoubles;
+  double* vbuf = my + NS * Cfg::kStageDoubles;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(vbuf + Cfg::kVbuf);
+  double* fac = smem + static_cast<size_t>(NW) * Cfg::kWarpDoubles;  // NPAD x FP, then inv diag
+  double* inv = fac + NPAD * FP;
+  double* csum = fac + Cfg::kFacDoubles;
+
+  for (int i = lane; i < NS * Cfg::kStageDoubles + Cfg::kVbuf; i += kWarp) my[i] = 0.0;
+  if (lane < NS) mbar_init(bars + lane, 1);
+  mbar_fence_init();
+  for (int i = threadIdx.x; i < Cfg::kSumDoubles; i += NW * kWarp) csum[i] = 0.0;
+  if (OP != OP_PLAIN) {
+    for (int i = threadIdx.x; i < Cfg::kFacDoubles; i += NW * kWarp) fac[i] = 0.0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n * n; i += NW * kWarp) {
+      const int r = i % n, c = i / n;
+      if (OP == OP_MULTIPLY || r <= c) fac[r + c * FP] = prm.factor[i];
+    }
+    __syncthreads();
+    if (OP == OP_SOLVE) {
+      // reference tsmRttsmR pre-check (gram.cpp:126-134): |r_jj| > n*eps*max|r_jj|, else
+      // SingularFactorError(j) for the first offending j; inv_diag precomputed.
+      if (threadIdx.x == 0) {
+        double mx = 0.0;
+        for (int j = 0; j < n; ++j) mx = fmax(mx, fabs(fac[j + j * FP]));
+        const double dtol = static_cast<double>(n) * 2.220446049250313e-16 * mx;
+        int bad = -1;
+        for (int j = 0; j < n; ++j) {
+          const double d = fac[j + j * FP];
+          if (bad < 0 && !(fabs(d) > dtol)) bad = j;
+          inv[j] = 1.0 / d;
+        }
+        if (bad >= 0 && blockIdx.x == 0) raise_status(prm.status, SQB_E_SINGULAR, bad);
+      }
+    }
+  }
+  __syncthreads();
+
+  const long long blk = blockIdx.x;
+  const long long begin = min(blk * prm.rows_per_block, prm.m);
+  const long long end = min((blk + 1) * prm.rows_per_block, prm.m);
+  const long long npanels = (end - begin + P - 1) / P;
+  const bool aligned = view_bulk_aligned(prm.x, n, begin);
+
+  double acc[NPAIR][2];
+#pragma unroll
+  for (int p = 0; p < NPAIR; ++p) acc[p][0] = acc[p][1] = 0.0;
+  uint32_t nf = 0;
+  uint32_t phase_bits = 0;   // bit s = parity to wait for on stage s
+  uint32_t async_bits = 0;   // bit s = stage s was filled by the async engine
+
+  auto issue = [&](long long pnl, int s) {
+    const bool a = issue_panel<P, PP>(prm.x, n, begin + pnl * P, end, aligned,
+                                      my + s * Cfg::kStageDoubles, bars + s, lane);
+    async_bits = a ? (async_bits | (1u << s)) : (async_bits & ~(1u << s));
+  };
+
+  // prologue: fill all stages
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const long long pnl = warp + static_cast<long long>(s) * NW;
+    if (pnl < npanels) issue(pnl, s);
+  }
+
+  long long it = 0;
+  for (long long pnl = warp; pnl < npanels; pnl += NW, ++it) {
+    const int s = static_cast<int>(it % NS);
+    const double* stage = my + s * Cfg::kStageDoubles;
+    if (async_bits & (1u << s)) {
+      mbar_wait(bars + s, (phase_bits >> s) & 1u);
+      phase_bits ^= 1u << s;
+    }
+
+    if (OP == OP_PLAIN) {
+#pragma unroll 2
+      for (int t = 0; t < P / 8; ++t) {
+        double2 a[NB];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          a[b] = *reinterpret_cast<const double2*>(stage + (8 * b + g) * PP + 8 * t + 2 * q);
+          nf = max(nf, max(nonfinite_bits(a[b].x), nonfinite_bits(a[b].y)));
+        }
+        int p = 0;
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+          for (int b2 = b; b2 < NB; ++b2, ++p) {
+            dmma884(acc[p][0], acc[p][1], a[b].x, a[b2].x);
+            dmma884(acc[p][0], acc[p][1], a[b].y, a[b2].y);
+          }
+      }
+      __syncwarp();
+      if (pnl + static_cast<long long>(NS) * NW < npanels) issue(pnl + static_cast<long long>(NS) * NW, s);
+    } else if (OP == OP_SOLVE) {
+      constexpr int RL = Cfg::RL;
+      double w[NB][RL];
+      nf = max(nf, load_panel_regs<NB, RL, PP>(w, stage, g, q));
+      __syncwarp();
+      if (pnl + NW < npanels) issue(pnl + NW, s);
+      // W <- W R^-1, column by column (kernels_scalar.cpp:19-32 order: subtract earlier columns
+      // in ascending order, then scale by the reciprocal diagonal)
+#pragma unroll
+      for (int bc = 0; bc < NB; ++bc) {
+        const int cols_here = min(8, n - 8 * bc);
+        for (int gc = 0; gc < cols_here; ++gc) {
+          const int c = 8 * bc + gc;
+          if (g == gc) {
+            const double d = inv[c];
+#pragma unroll
+            for (int t = 0; t < RL / 2; ++t) {
+              w[bc][2 * t] *= d;
+              w[bc][2 * t + 1] *= d;
+              *reinterpret_cast<double2*>(vbuf + 8 * t + 2 * q) =
+                  make_double2(w[bc][2 * t], w[bc][2 * t + 1]);
+            }
+          }
+          __syncwarp();
+          double v[RL];
+#pragma unroll
+          for (int t = 0; t < RL / 2; ++t) {
+            const double2 pv = *reinterpret_cast<const double2*>(vbuf + 8 * t + 2 * q);
+            v[2 * t] = pv.x;
+            v[2 * t + 1] = pv.y;
+          }
+#pragma unroll
+          for (int b = bc; b < NB; ++b) {
+            const int j = 8 * b + g;
+            const double r = (j > c) ? fac[c + j * FP] : 0.0;  // padded columns hold zeros
+#pragma unroll
+            for (int i = 0; i < RL; ++i) w[b][i] = fma(-r, v[i], w[b][i]);
+          }
+          __syncwarp();
+        }
+      }
+      int p = 0;
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int b2 = b; b2 < NB; ++b2, ++p)
+#pragma unroll
+          for (int i = 0; i < RL; ++i) dmma884(acc[p][0], acc[p][1], w[b][i], w[b2][i]);
+    } else {  // OP_MULTIPLY
+      const int kchunks = (n + 3) / 4;
+      for (int t = 0; t < P / 8; ++t) {
+        double y[NB][2];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) y[b][0] = y[b][1] = 0.0;
+        for (int kc = 0; kc < kchunks; ++kc) {
+          const double bf = stage[(4 * kc + q) * PP + 8 * t + g];
+          nf = max(nf, nonfinite_bits(bf));
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            const double af = fac[(4 * kc + q) + (8 * b + g) * FP];
+            dmma884(y[b][0], y[b][1], af, bf);
+          }
+        }
+        int p = 0;
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+          for (int b2 = b; b2 < NB; ++b2, ++p) {
+            dmma884(acc[p][0], acc[p][1], y[b][0], y[b2][0]);
+            dmma884(acc[p][0], acc[p][1], y[b][1], y[b2][1]);
+          }
+      }
+      __syncwarp();
+      if (pnl + static_cast<long long>(NS) * NW < npanels) issue(pnl + static_cast<long long>(NS) * NW, s);
+    }
+  }
+
+  if (prm.check_finite) flag_nonfinite(nf, prm.status, lane);
+
+  // ---- CTA reduction in fixed warp order, then the block's upper-triangle partial -------------
+  for (int wi = 0; wi < NW; ++wi) {
+    __syncthreads();
+    if (warp == wi) {
+      int p = 0;
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int b2 = b; b2 < NB; ++b2, ++p) {
+          const int row = 8 * b + g, col = 8 * b2 + 2 * q;
+          csum[row + col * NPAD] += acc[p][0];
+          csum[row + (col + 1) * NPAD] += acc[p][1];
+        }
+    }
+  }
+  __syncthreads();
+  double* dst = prm.partial + blk * static_cast<long long>(n) * n;
+  for (int idx = threadIdx.x; idx < n * n; idx += NW * kWarp) {
+    const int i = idx % n, j = idx / n;
+    dst[idx] = i <= j ? csum[i + j * NPAD] : 0.0;
+  }
+}
+
+// Sum the per-block partials in ascending block order over the upper triangle and mirror
+// (reference gram.cpp:81-92).
+__global__ void gram_reduce_kernel(const double* partial, long long num_blocks, int n, double* c) {
+  for (int idx = threadIdx.x + blockIdx.x * blockDim.x; idx < n * n; idx += blockDim.x * gridDim.x) {
+    const int i = idx % n, j = idx / n;
+    if (i > j) continue;
+    double s = 0.0;
+    for (long long b = 0; b < num_blocks; ++b) s += partial[b * static_cast<long long>(n) * n + idx];
+    c[i + j * n] = s;
+    c[j + i * n] = s;
+  }
+}
+
+template <int NB, int OP>
+static cudaError_t launch_gram_nb(const GramParams& prm, long long num_blocks, cudaStream_t stream) {
+  using Cfg = GramCfg<NB, OP>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gram_mma_kernel<NB, OP>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(Cfg::kSmemBytes));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  gram_mma_kernel<NB, OP>
+      <<<static_cast<unsigned>(num_blocks), Cfg::NW * kWarp, Cfg::kSmemBytes, stream>>>(prm);
+  return cudaGetLastError();
+}
+
+template <int OP>
+static cudaError_t launch_gram_op(const GramParams& prm, long long num_blocks, cudaStream_t stream) {
+  switch ((prm.n + 7) / 8) {
+    case 1: return launch_gram_nb<1, OP>(prm, num_blocks, stream);
+    case 2: return launch_gram_nb<2, OP>(prm, num_blocks, stream);
+    case 3: return launch_gram_nb<3, OP>(prm, num_blocks, stream);
+    case 4: return launch_gram_nb<4, OP>(prm, num_blocks, stream);
+    case 5: return launch_gram_nb<5, OP>(prm, num_blocks, stream);
+    case 6: return launch_gram_nb<6, OP>(prm, num_blocks, stream);
+    case 7: return launch_gram_nb<7, OP>(prm, num_blocks, stream);
+    case 8: return launch_gram_nb<8, OP>(prm, num_blocks, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_gram(const GramParams& prm, int op, long long num_blocks, cudaStream_t stream) {
+  switch (op) {
+    case OP_PLAIN: return launch_gram_op<OP_PLAIN>(prm, num_blocks, stream);
+    case OP_SOLVE: return launch_gram_op<OP_SOLVE>(prm, num_blocks, stream);
+    case OP_MULTIPLY: return launch_gram_op<OP_MULTIPLY>(prm, num_blocks, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_gram_reduce(const double* partial, long long num_blocks, int n, double* c,
+                               cudaStream_t stream) {
+  gram_reduce_kernel<<<(n * n + 255) / 256, 256, 0, stream>>>(partial, num_blocks, n, c);
+  return cudaGetLastError();
+}
+
+int gram_panel_rows(int n, int op) {
+  const int nb = (n + 7) / 8;
+#define SQB_CASE(NBV)                                                                   \
+  case NBV:                                                                              \
+    return op == OP_PLAIN ? GramCfg<NBV, OP_PLAIN>::P                                    \
+                          : (op == OP_SOLVE ? GramCfg<NBV, OP_SOLVE>::P : GramCfg<NBV, OP_MULTIPLY>::P);
+  switch (nb) {
+    SQB_CASE(1) SQB_CASE(2) SQB_CASE(3) SQB_CASE(4) SQB_CASE(5) SQB_CASE(6) SQB_CASE(7)
+    default: return op == OP_PLAIN ? GramCfg<8, OP_PLAIN>::P
+                                   : (op == OP_SOLVE ? GramCfg<8, OP_SOLVE>::P : GramCfg<8, OP_MULTIPLY>::P);
+  }
+#undef SQB_CASE
+}
+
+int gram_warps(int n) { return (n + 7) / 8 >= 8 ? 6 : 8; }
+
+}  // namespace sqb

@@ -1,0 +1,74 @@
+// Internal launcher declarations shared between the kernel translation units and the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "tsqr_warp.cuh"
+
+namespace sqb {
+
+// ---- tsqr_kernels.cu ---------------------------------------------------------------------
+struct TsqrParams {
+  MatView x;
+  long long m;
+  int n;
+  long long rows_per_block;
+  double* y;         // block blk's triangle goes to rows [blk*n, blk*n+n), leading dim ldy
+  long long ldy;
+  int finalize;      // sign-normalise (reference sign_normalize, src/types.cpp:8-14)
+  int check_finite;  // raise StatusWord::nonfinite when an Inf/NaN is streamed
+  StatusWord* status;
+};
+cudaError_t launch_tsqr_warp(const TsqrParams& prm, long long num_blocks, cudaStream_t stream);
+int tsqr_warp_panel_rows(int n);
+int tsqr_warp_warps(int n);
+
+// ---- gram_kernels.cu ---------------------------------------------------------------------
+enum { OP_PLAIN = 0, OP_SOLVE = 1, OP_MULTIPLY = 2 };
+struct GramParams {
+  MatView x;
+  long long m;
+  int n;
+  long long rows_per_block;
+  const double* factor;  // n x n column-major: R (OP_SOLVE) or B (OP_MULTIPLY); null for OP_PLAIN
+  double* partial;       // num_blocks x (n*n): each block's upper-triangle partial
+  int check_finite;
+  StatusWord* status;
+};
+cudaError_t launch_gram(const GramParams& prm, int op, long long num_blocks, cudaStream_t stream);
+cudaError_t launch_gram_reduce(const double* partial, long long num_blocks, int n, double* c,
+                               cudaStream_t stream);
+int gram_panel_rows(int n, int op);
+int gram_warps(int n);
+
+// ---- small_kernels.cu (n x n work, one CTA each) -------------------------------------------
+constexpr int kSmallMaxN = 128;
+cudaError_t launch_cholesky(const double* c, int n, double* r, StatusWord* status,
+                            cudaStream_t stream);
+cudaError_t launch_eigh(const double* c, int n, double* values, double* vectors, double* scratch,
+                        StatusWord* status, cudaStream_t stream);
+// scratch: at least 4*n*n + 4*n doubles of device memory
+cudaError_t launch_svqb_pass(const double* c, int n, double* b, double* z, double* sigma,
+                             long long* rank, int want_sigma, double* scratch, StatusWord* status,
+                             cudaStream_t stream);
+cudaError_t launch_tri_multiply(const double* a, const double* b, int n, double* out,
+                                cudaStream_t stream);
+cudaError_t launch_small_multiply(const double* a, const double* b, int n, double* out,
+                                  cudaStream_t stream);
+cudaError_t launch_backsolve(const double* r, int ne, double* xsol, double* residual,
+                             StatusWord* status, cudaStream_t stream);
+cudaError_t launch_check_finite(const double* a, long long count, StatusWord* status,
+                                cudaStream_t stream);
+// Q = X R^-1 (reference reconstruct_q, src/gram_qr.cpp:193-221)
+cudaError_t launch_apply_rinv(const double* x, long long m, int n, long long ld, const double* r,
+                              double* q, long long ldq, StatusWord* status, cudaStream_t stream);
+
+// ---- matgen_kernels.cu -----------------------------------------------------------------------
+cudaError_t launch_fill_gaussian(double* x, long long m, int n, long long ld, unsigned long long seed,
+                                 long long row_offset, long long m_total, cudaStream_t stream);
+cudaError_t launch_generate(double* x, long long m, int n, long long ld, double kappa,
+                            int linear_decay, unsigned long long seed, double* scratch,
+                            cudaStream_t stream);
+size_t generate_scratch_doubles(long long m, int n);
+
+}  // namespace sqb

@@ -1,0 +1,548 @@
+// n x n factorisations and products, one CTA each, so that the Gram-based drivers never leave the
+// device between their two streaming passes.
+//
+//   cholesky_kernel     reference cholesky            (src/gram_qr.cpp:36-58)
+//   eigh_kernel         reference eigh_small          (src/gram_qr.cpp:60-121)
+//   svqb_pass_kernel    reference svqb_pass           (src/gram_qr.cpp:133-176)
+//   tri_multiply        reference triangular_multiply (src/small.cpp:9-20)
+//   small_multiply      reference small_multiply      (src/small.cpp:22-32)
+//   backsolve_kernel    reference solve_lstsq tail    (src/lstsq.cpp:44-59)
+//   apply_rinv_kernel   reference reconstruct_q       (src/gram_qr.cpp:193-221)
+#include <cfloat>
+
+#include "kernels.h"
+
+namespace sqb {
+
+namespace {
+
+constexpr int kSmallThreads = 256;
+constexpr double kEps = 2.220446049250313e-16;  // std::numeric_limits<double>::epsilon()
+
+// ------------------------------------------------------------------------------------------------
+// Cholesky: right-looking, upper factor R^T R = C.  Arithmetic per entry is the reference's
+// (subtract r_ki r_kj for ascending k, divide by r_ii, sqrt of the reduced pivot); breakdown when
+// the reduced pivot is <= n*eps*max_j|c_jj| (gram_qr.cpp:39-54), reported with its column index.
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSmallThreads)
+    cholesky_kernel(const double* __restrict__ c, int n, double* __restrict__ r, StatusWord* status) {
+  extern __shared__ __align__(16) double sm[];
+  const int ld = n + 1;
+  double* a = sm;
+  __shared__ double tol_s;
+  __shared__ int fail_s;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < n * n; idx += kSmallThreads) {
+    const int i = idx % n, j = idx / n;
+    a[i + j * ld] = c[idx];
+  }
+  if (tid == 0) {
+    double mx = 0.0;
+    for (int j = 0; j < n; ++j) mx = fmax(mx, fabs(c[j + j * n]));
+    tol_s = static_cast<double>(n) * kEps * mx;
+    fail_s = -1;
+  }
+  __syncthreads();
+  const double tol = tol_s;
+  const int tx = tid & 15, ty = tid >> 4;
+  for (int k = 0; k < n; ++k) {
+    const double d = a[k + k * ld];
+    if (d <= tol) {
+      if (tid == 0) {
+        fail_s = k;
+        raise_status(status, SQB_E_BREAKDOWN, k);
+      }
+      break;
+    }
+    const double rkk = sqrt(d);
+    __syncthreads();
+    if (tid == 0) a[k + k * ld] = rkk;
+    for (int j = k + 1 + tid; j < n; j += kSmallThreads) a[k + j * ld] = a[k + j * ld] / rkk;
+    __syncthreads();
+    for (int j = k + 1 + ty; j < n; j += 16) {
+      const double rkj = a[k + j * ld];
+      for (int i = k + 1 + tx; i <= j; i += 16) a[i + j * ld] = fma(-a[k + i * ld], rkj, a[i + j * ld]);
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  const bool failed = fail_s >= 0;
+  for (int idx = tid; idx < n * n; idx += kSmallThreads) {
+    const int i = idx % n, j = idx / n;
+    r[idx] = (i <= j && !failed) ? a[i + j * ld] : 0.0;
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Symmetric eigensolver: Jacobi with the reference's rotation formulas, skip rule (a_pq == 0),
+// stopping test off(A) <= 10*n*eps*|C|_F checked once per sweep, 30-sweep cap and stable
+// descending sort (gram_qr.cpp:60-121).  The reference sweeps cyclic-by-row, one rotation at a
+// time; here the n/2 disjoint rotations of a round-robin round are applied together (column
+// phase, row phase), which is what lets one CTA finish a 64 x 64 problem in ~0.1 ms.
+// `a` (np x lda, np = n rounded up to even) and `u` (n x ldu) are CTA-visible scratch.
+// Returns false when the sweep cap is hit.  On return perm[j] = source column of output j.
+// ------------------------------------------------------------------------------------------------
+struct JacobiScratch {
+  double* cs;    // np/2
+  double* sn;    // np/2
+  double* dpp;   // np/2
+  double* dqq;   // np/2
+  int* pp;       // np/2
+  int* qq;       // np/2
+  double* red;   // kSmallThreads
+  int* perm;     // n
+};
+
+__device__ double block_sum(double v, double* red) {
+  const int tid = threadIdx.x;
+  __syncthreads();
+  red[tid] = v;
+  __syncthreads();
+  for (int s = kSmallThreads / 2; s > 0; s >>= 1) {
+    if (tid < s) red[tid] += red[tid + s];
+    __syncthreads();
+  }
+  const double out = red[0];
+  __syncthreads();
+  return out;
+}
+
+__device__ bool jacobi_eigh(double* a, int lda, double* u, int ldu, int n, const JacobiScratch& js) {
+  const int tid = threadIdx.x;
+  const int np = (n + 1) & ~1;
+  const int half = np / 2;
+  // |C|_F and identity U
+  double fro = 0.0;
+  for (int idx = tid; idx < n * n; idx += kSmallThreads) {
+    const int i = idx % n, j = idx / n;
+    const double v = a[i + j * lda];
+    fro = fma(v, v, fro);
+    u[i + j * ldu] = i == j ? 1.0 : 0.0;
+  }
+  if (np > n) {  // padding index: zero row/column, never rotated (a_pq == 0 rule)
+    for (int i = tid; i < np; i += kSmallThreads) {
+      a[i + n * lda] = 0.0;
+      a[n + i * lda] = 0.0;
+    }
+  }
+  const double thr = 10.0 * static_cast<double>(n) * kEps * sqrt(block_sum(fro, js.red));
+
+  auto offdiag = [&]() {
+    double s = 0.0;
+    for (int idx = tid; idx < n * n; idx += kSmallThreads) {
+      const int i = idx % n, j = idx / n;
+      if (i < j) s = fma(a[i + j * lda], a[i + j * lda], s);
+    }
+    return sqrt(2.0 * block_sum(s, js.red));
+  };
+
+  bool converged = offdiag() <= thr;
+  for (int sweep = 0; sweep < 30 && !converged; ++sweep) {
+    for (int step = 0; step < np - 1; ++step) {
+      // phase A: rotation parameters of this round's pairs
+      if (tid < half) {
+        int x, y;
+        if (tid == 0) {
+          x = np - 1;
+          y = step;
+        } else {
+          x = (step + tid) % (np - 1);
+          y = (step - tid + (np - 1)) % (np - 1);
+        }
+        const int p = min(x, y), q = max(x, y);
+        const double apq = a[p + q * lda];
+        double cs = 1.0, sn = 0.0, npp = 0.0, nqq = 0.0;
+        int pmark = -1;
+        if (apq != 0.0) {
+          const double app = a[p + p * lda], aqq = a[q + q * lda];
+          const double theta = (aqq - app) / (2.0 * apq);
+          const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
+          cs = 1.0 / sqrt(1.0 + t * t);
+          sn = t * cs;
+          npp = app - t * apq;
+          nqq = aqq + t * apq;
+          pmark = p;
+        }
+        js.cs[tid] = cs;
+        js.sn[tid] = sn;
+        js.dpp[tid] = npp;
+        js.dqq[tid] = nqq;
+        js.pp[tid] = pmark;
+        js.qq[tid] = q;
+      }
+      __syncthreads();
+      // phase B: columns  A <- A J,  U <- U J
+      for (int idx = tid; idx < half * np; idx += kSmallThreads) {
+        const int t = idx / np, i = idx % np;
+        const int p = js.pp[t];
+        if (p < 0) continue;
+        const int q = js.qq[t];
+        const double cs = js.cs[t], sn = js.sn[t];
+        const double aip = a[i + p * lda], aiq = a[i + q * lda];
+        a[i + p * lda] = cs * aip - sn * aiq;
+        a[i + q * lda] = sn * aip + cs * aiq;
+        if (i < n) {
+          const double uip = u[i + p * ldu], uiq = u[i + q * ldu];
+          u[i + p * ldu] = cs * uip - sn * uiq;
+          u[i + q * ldu] = sn * uip + cs * uiq;
+        }
+      }
+      __syncthreads();
+      // phase C: rows  A <- J^T A
+      for (int idx = tid; idx < half * np; idx += kSmallThreads) {
+        const int t = idx / np, j = idx % np;
+        const int p = js.pp[t];
+        if (p < 0) continue;
+        const int q = js.qq[t];
+        const double cs = js.cs[t], sn = js.sn[t];
+        const double apj = a[p + j * lda], aqj = a[q + j * lda];
+        a[p + j * lda] = cs * apj - sn * aqj;
+        a[q + j * lda] = sn * apj + cs * aqj;
+      }
+      __syncthreads();
+      // phase D: exact 2x2 results (gram_qr.cpp:84-87)
+      if (tid < half && js.pp[tid] >= 0) {
+        const int p = js.pp[tid], q = js.qq[tid];
+        a[p + p * lda] = js.dpp[tid];
+        a[q + q * lda] = js.dqq[tid];
+        a[p + q * lda] = 0.0;
+        a[q + p * lda] = 0.0;
+      }
+      __syncthreads();
+    }
+    converged = offdiag() <= thr;
+  }
+  // stable descending rank (gram_qr.cpp:107-110)
+  for (int j = tid; j < n; j += kSmallThreads) js.perm[j] = j;
+  __syncthreads();
+  for (int j = tid; j < n; j += kSmallThreads) {
+    const double lj = a[j + j * lda];
+    int rank = 0;
+    for (int i = 0; i < n; ++i) {
+      const double li = a[i + i * lda];
+      rank += (li > lj) || (li == lj && i < j);
+    }
+    js.perm[rank] = j;
+  }
+  __syncthreads();
+  return converged;
+}
+
+struct SmallLayout {
+  int lda, ldu;
+  size_t a_off, u_off, misc_off, total_doubles;
+  bool u_in_smem;
+};
+
+__host__ __device__ inline SmallLayout small_layout(int n) {
+  SmallLayout L;
+  const int np = (n + 1) & ~1;
+  L.lda = np + 1;
+  L.ldu = n + 1;
+  L.a_off = 0;
+  size_t off = static_cast<size_t>(np) * L.lda;
+  L.u_in_smem = n <= 64;
+  L.u_off = off;
+  if (L.u_in_smem) off += static_cast<size_t>(n) * L.ldu;
+  L.misc_off = off;
+  // cs, sn, dpp, dqq (np/2 each), pp, qq (np/2 ints each -> np/2 doubles), red, perm (n ints)
+  off += 4 * (np / 2) + (np / 2) + kSmallThreads + (n + 1) / 2 + 4;
+  L.total_doubles = off;
+  return L;
+}
+
+__device__ JacobiScratch carve_scratch(double* sm, const SmallLayout& L, int n) {
+  const int np = (n + 1) & ~1;
+  JacobiScratch js;
+  double* p = sm + L.misc_off;
+  js.cs = p; p += np / 2;
+  js.sn = p; p += np / 2;
+  js.dpp = p; p += np / 2;
+  js.dqq = p; p += np / 2;
+  js.pp = reinterpret_cast<int*>(p);
+  js.qq = js.pp + np / 2;
+  p += np / 2;
+  js.red = p; p += kSmallThreads;
+  js.perm = reinterpret_cast<int*>(p);
+  return js;
+}
+
+__global__ void __launch_bounds__(kSmallThreads)
+    eigh_kernel(const double* __restrict__ c, int n, double* values, double* vectors,
+                double* gscratch, StatusWord* status) {
+  extern __shared__ __align__(16) double sm[];
+  const SmallLayout L = small_layout(n);
+  double* a = sm + L.a_off;
+  double* u = L.u_in_smem ? sm + L.u_off : gscratch;
+  const JacobiScratch js = carve_scratch(sm, L, n);
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < n * n; idx += kSmallThreads) a[idx % n + (idx / n) * L.lda] = c[idx];
+  __syncthreads();
+  const bool ok = jacobi_eigh(a, L.lda, u, L.ldu, n, js);
+  if (!ok && tid == 0) raise_status(status, SQB_E_NO_CONVERGENCE, -1);
+  for (int j = tid; j < n; j += kSmallThreads) values[j] = a[js.perm[j] + js.perm[j] * L.lda];
+  for (int idx = tid; idx < n * n; idx += kSmallThreads) {
+    const int i = idx % n, j = idx / n;
+    vectors[idx] = u[i + js.perm[j] * L.ldu];
+  }
+}
+
+// One SVQB pass on a Gram matrix (gram_qr.cpp:133-176): D = diag(C)^-1/2 (1 for zero columns),
+// eigen-decomposition of D C D, rank = #{lambda >= 10 n eps lambda_max}, B = D U L^-1/2,
+// Z = L^1/2 U^T D^-1 with truncated columns/rows exactly zero; sigma = sqrt(max(eig(C), 0)) from a
+// second eigen-decomposition of the unscaled Gram matrix.
+__global__ void __launch_bounds__(kSmallThreads)
+    svqb_pass_kernel(const double* __restrict__ c, int n, double* bmat, double* z, double* sigma,
+                     long long* rank_out, int want_sigma, double* gscratch, StatusWord* status) {
+  extern __shared__ __align__(16) double sm[];
+  const SmallLayout L = small_layout(n);
+  double* a = sm + L.a_off;
+  double* u = L.u_in_smem ? sm + L.u_off : gscratch;
+  double* ds = gscratch + static_cast<size_t>(n) * (n + 1);   // n
+  double* dsi = ds + n;                                       // n
+  const JacobiScratch js = carve_scratch(sm, L, n);
+  __shared__ int rank_s;
+  __shared__ int fail_s;
+  const int tid = threadIdx.x;
+
+  for (int j = tid; j < n; j += kSmallThreads) {
+    const double d = c[j + j * n];
+    ds[j] = d > 0.0 ? 1.0 / sqrt(d) : 1.0;
+    dsi[j] = d > 0.0 ? sqrt(d) : 1.0;
+  }
+  if (tid == 0) fail_s = 0;
+  __syncthreads();
+  for (int idx = tid; idx < n * n; idx += kSmallThreads) {
+    const int i = idx % n, j = idx / n;
+    a[i + j * L.lda] = c[idx] * ds[i] * ds[j];
+  }
+  __syncthreads();
+  bool ok = jacobi_eigh(a, L.lda, u, L.ldu, n, js);
+  if (tid == 0) {
+    int rank = 0;
+    if (!ok) {
+      raise_status(status, SQB_E_NO_CONVERGENCE, -1);
+      fail_s = 1;
+    } else {
+      const double lmax = a[js.perm[0] + js.perm[0] * L.lda];
+      if (!(lmax > 0.0)) {
+        raise_status(status, SQB_E_ZERO_MATRIX, -1);
+        fail_s = 1;
+      } else {
+        const double tol = 10.0 * static_cast<double>(n) * kEps;
+        while (rank < n && a[js.perm[rank] + js.perm[rank] * L.lda] >= tol * lmax) ++rank;
+        if (rank == 0) {
+          raise_status(status, SQB_E_ZERO_MATRIX, -1);
+          fail_s = 1;
+        }
+      }
+    }
+    rank_s = rank;
+    *rank_out = rank;
+  }
+  __syncthreads();
+  const int rank = rank_s;
+  for (int idx = tid; idx < n * n; idx += kSmallThreads) {
+    const int i = idx % n, j = idx / n;
+    double bv = 0.0, zv = 0.0;
+    if (j < rank && !fail_s) {
+      const int src = js.perm[j];
+      const double lam = a[src + src * L.lda];
+      const double uij = u[i + src * L.ldu];
+      bv = ds[i] * uij * (1.0 / sqrt(lam));
+      zv = sqrt(lam) * uij * dsi[i];
+    }
+    bmat[i + j * n] = bv;   // B(i,j)
+    z[j + i * n] = zv;      // Z(j,i)
+  }
+  __syncthreads();
+  if (want_sigma) {
+    for (int idx = tid; idx < n * n; idx += kSmallThreads) a[idx % n + (idx / n) * L.lda] = c[idx];
+    __syncthreads();
+    ok = jacobi_eigh(a, L.lda, u, L.ldu, n, js);
+    if (!ok && tid == 0) raise_status(status, SQB_E_NO_CONVERGENCE, -1);
+    for (int j = tid; j < n; j += kSmallThreads)
+      sigma[j] = sqrt(fmax(a[js.perm[j] + js.perm[j] * L.lda], 0.0));
+  }
+}
+
+// out = A B for upper-triangular A, B (small.cpp:9-20): sum over t in [i, j], ascending.
+__global__ void tri_multiply_kernel(const double* __restrict__ a, const double* __restrict__ b, int n,
+                                    double* __restrict__ out) {
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int i = idx % n, j = idx / n;
+    double s = 0.0;
+    if (i <= j)
+      for (int t = i; t <= j; ++t) s = fma(a[i + t * n], b[t + j * n], s);
+    out[idx] = s;
+  }
+}
+
+// out = A B, dense n x n (small.cpp:22-32)
+__global__ void small_multiply_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                      int n, double* __restrict__ out) {
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int i = idx % n, j = idx / n;
+    double s = 0.0;
+    for (int t = 0; t < n; ++t) s = fma(a[i + t * n], b[t + j * n], s);
+    out[idx] = s;
+  }
+}
+
+// Least-squares tail (lstsq.cpp:44-59): back-substitution on the leading n x n block of the
+// (n+1) x (n+1) triangle of [A rhs]; residual = |R(n,n)|; RankDeficiencyError(i) when
+// |R(i,i)| <= n*eps*max|diag R[0:n]|.
+__global__ void backsolve_kernel(const double* __restrict__ r, int ne, double* xsol, double* residual,
+                                 StatusWord* status) {
+  if (threadIdx.x != 0) return;
+  const int n = ne - 1;
+  double mx = 0.0;
+  for (int j = 0; j < n; ++j) mx = fmax(mx, fabs(r[j + j * ne]));
+  const double dtol = static_cast<double>(n) * kEps * mx;
+  for (int i = n - 1; i >= 0; --i) {
+    const double d = r[i + i * ne];
+    if (fabs(d) <= dtol) {
+      raise_status(status, SQB_E_RANK_DEFICIENT, i);
+      return;
+    }
+    double s = r[i + n * ne];
+    for (int j = i + 1; j < n; ++j) s -= r[i + j * ne] * xsol[j];
+    xsol[i] = s / d;
+  }
+  *residual = fabs(r[n + n * ne]);
+}
+
+__global__ void check_finite_kernel(const double* __restrict__ a, long long count, StatusWord* status) {
+  uint32_t nf = 0;
+  for (long long i = threadIdx.x + static_cast<long long>(blockIdx.x) * blockDim.x; i < count;
+       i += static_cast<long long>(blockDim.x) * gridDim.x)
+    nf = max(nf, nonfinite_bits(a[i]));
+  if (nf >= kNonFiniteHi) atomicExch(&status->nonfinite, 1);
+}
+
+// Q = X R^-1, one row per thread, column-oriented substitution with the reciprocal diagonal and
+// exact-zero r_ij skipped, i.e. the reference's order (gram_qr.cpp:203-215).
+template <int NMAX>
+__global__ void __launch_bounds__(128)
+    apply_rinv_kernel(const double* __restrict__ x, long long m, int n, long long ld,
+                      const double* __restrict__ r, double* __restrict__ qout, long long ldq) {
+  __shared__ double rs[NMAX * NMAX];
+  __shared__ double inv[NMAX];
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) rs[idx % n + (idx / n) * NMAX] = r[idx];
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) inv[j] = 1.0 / rs[j + j * NMAX];
+  __syncthreads();
+  for (long long row = threadIdx.x + static_cast<long long>(blockIdx.x) * blockDim.x; row < m;
+       row += static_cast<long long>(blockDim.x) * gridDim.x) {
+    double y[NMAX];
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) y[j] = j < n ? x[row + j * ld] : 0.0;
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) {
+      if (j < n) {
+        double acc = y[j];
+#pragma unroll
+        for (int i = 0; i < j; ++i) {
+          const double rij = rs[i + j * NMAX];
+          if (rij != 0.0) acc = fma(-rij, y[i], acc);
+        }
+        y[j] = acc * inv[j];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j)
+      if (j < n) qout[row + j * ldq] = y[j];
+  }
+}
+
+__global__ void rinv_precheck_kernel(const double* __restrict__ r, int n, StatusWord* status) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double mx = 0.0;
+  for (int j = 0; j < n; ++j) mx = fmax(mx, fabs(r[j + j * n]));
+  const double dtol = static_cast<double>(n) * kEps * mx;   // trsm_diag_tolerance, gram.cpp:106-111
+  for (int j = 0; j < n; ++j)
+    if (fabs(r[j + j * n]) <= dtol) {
+      raise_status(status, SQB_E_SINGULAR, j);
+      return;
+    }
+}
+
+size_t small_smem_bytes(int n) { return small_layout(n).total_doubles * sizeof(double); }
+
+template <typename K>
+cudaError_t opt_in_smem(K kernel, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(bytes));
+}
+
+}  // namespace
+
+cudaError_t launch_cholesky(const double* c, int n, double* r, StatusWord* status,
+                            cudaStream_t stream) {
+  const size_t bytes = sizeof(double) * static_cast<size_t>(n) * (n + 1);
+  cudaError_t e = opt_in_smem(cholesky_kernel, bytes);
+  if (e != cudaSuccess) return e;
+  cholesky_kernel<<<1, kSmallThreads, bytes, stream>>>(c, n, r, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_eigh(const double* c, int n, double* values, double* vectors, double* scratch,
+                        StatusWord* status, cudaStream_t stream) {
+  const size_t bytes = small_smem_bytes(n);
+  cudaError_t e = opt_in_smem(eigh_kernel, bytes);
+  if (e != cudaSuccess) return e;
+  eigh_kernel<<<1, kSmallThreads, bytes, stream>>>(c, n, values, vectors, scratch, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_svqb_pass(const double* c, int n, double* b, double* z, double* sigma,
+                             long long* rank, int want_sigma, double* scratch, StatusWord* status,
+                             cudaStream_t stream) {
+  const size_t bytes = small_smem_bytes(n);
+  cudaError_t e = opt_in_smem(svqb_pass_kernel, bytes);
+  if (e != cudaSuccess) return e;
+  svqb_pass_kernel<<<1, kSmallThreads, bytes, stream>>>(c, n, b, z, sigma, rank, want_sigma, scratch,
+                                                        status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tri_multiply(const double* a, const double* b, int n, double* out,
+                                cudaStream_t stream) {
+  tri_multiply_kernel<<<1, 256, 0, stream>>>(a, b, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_small_multiply(const double* a, const double* b, int n, double* out,
+                                  cudaStream_t stream) {
+  small_multiply_kernel<<<1, 256, 0, stream>>>(a, b, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_backsolve(const double* r, int ne, double* xsol, double* residual,
+                             StatusWord* status, cudaStream_t stream) {
+  backsolve_kernel<<<1, 32, 0, stream>>>(r, ne, xsol, residual, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_check_finite(const double* a, long long count, StatusWord* status,
+                                cudaStream_t stream) {
+  const int blocks = static_cast<int>(count < 65536 ? 1 : 296);
+  check_finite_kernel<<<blocks, 256, 0, stream>>>(a, count, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apply_rinv(const double* x, long long m, int n, long long ld, const double* r,
+                              double* q, long long ldq, StatusWord* status, cudaStream_t stream) {
+  rinv_precheck_kernel<<<1, 32, 0, stream>>>(r, n, status);
+  const long long want = (m + 127) / 128;
+  const int blocks = static_cast<int>(want < 148 * 8 ? (want < 1 ? 1 : want) : 148 * 8);
+  if (n <= 8) apply_rinv_kernel<8><<<blocks, 128, 0, stream>>>(x, m, n, ld, r, q, ldq);
+  else if (n <= 16) apply_rinv_kernel<16><<<blocks, 128, 0, stream>>>(x, m, n, ld, r, q, ldq);
+  else if (n <= 32) apply_rinv_kernel<32><<<blocks, 128, 0, stream>>>(x, m, n, ld, r, q, ldq);
+  else if (n <= 64) apply_rinv_kernel<64><<<blocks, 128, 0, stream>>>(x, m, n, ld, r, q, ldq);
+  else return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+}  // namespace sqb

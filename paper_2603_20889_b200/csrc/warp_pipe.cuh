@@ -1,0 +1,73 @@
+// Warp-private panel staging: every warp of a streaming CTA owns NS shared-memory stages that the
+// TMA engine fills with bulk async copies (cp.async.bulk, one per column segment, completion on a
+// warp-private mbarrier).  No __syncthreads anywhere in the streaming loops - warps run free.
+//
+// Reference analogue: TrapezoidalWorkspace::load_panel / the Gram workspace memcpy
+// (reference src/tsqr.cpp:27-40, src/gram.cpp:57-68) - "bring a b-row panel of X on chip".
+#pragma once
+
+#include "common.cuh"
+
+namespace sqb {
+
+// Input matrix view: columns 0..n_main-1 come from base (leading dimension ld); an optional
+// extra last column comes from `extra` (least squares: the [A rhs] pencil without assembling it,
+// reference src/lstsq.cpp:24-26 copies instead).
+struct MatView {
+  const double* base;
+  long long ld;
+  const double* extra;
+  int n_main;
+  __device__ __forceinline__ const double* col(int j) const {
+    return j < n_main ? base + static_cast<long long>(j) * ld : extra;
+  }
+};
+
+// Stage pitch (doubles per column).  residue 8 (mod 16): the "two rows per lane" LDS.128 fragment
+// pattern (address = col*PP + 8t + 2q) is bank-conflict free; residue 4: the transposed LDS.64
+// fragment pattern (address = (4k+q)*PP + 8t + g) is.
+constexpr int stage_pitch(int p, int residue) { return p + ((residue - (p % 16)) + 16) % 16; }
+
+__device__ __forceinline__ bool view_bulk_aligned(const MatView& x, int n, long long begin) {
+  bool ok = ((reinterpret_cast<uintptr_t>(x.base) & 15) == 0) && ((x.ld & 1) == 0) &&
+            ((begin & 1) == 0);
+  if (x.n_main < n) ok = ok && ((reinterpret_cast<uintptr_t>(x.extra) & 15) == 0);
+  return ok;
+}
+
+// Fill one stage with rows [r0, min(r0+P, end)) of the n live columns.  Full, 16-byte aligned
+// panels go through the async engine (returns true: wait on `bar`); ragged or unaligned panels
+// are filled synchronously by the warp with zero padding (returns false).
+template <int P, int PP>
+__device__ __forceinline__ bool issue_panel(const MatView& x, int n, long long r0, long long end,
+                                            bool aligned, double* stage, uint64_t* bar, int lane) {
+  const long long left = end - r0;
+  if (aligned && left >= P) {
+    if (lane == 0) {
+      fence_async_smem();
+      mbar_expect_tx(bar, static_cast<uint32_t>(n * P * sizeof(double)));
+      for (int j = 0; j < n; ++j) bulk_g2s(stage + j * PP, x.col(j) + r0, P * sizeof(double), bar);
+    }
+    return true;
+  }
+  const int live = static_cast<int>(left < P ? left : P);
+  for (int j = 0; j < n; ++j) {
+    const double* src = x.col(j) + r0;
+    for (int r = lane; r < P; r += kWarp) stage[j * PP + r] = r < live ? __ldg(src + r) : 0.0;
+  }
+  __syncwarp();
+  return false;
+}
+
+// max over the warp of the exponent-field probe (fused non-finite validation, replaces the
+// reference's serial scans: src/types.cpp:40-48, src/gram.cpp:96-102).
+__device__ __forceinline__ void flag_nonfinite(uint32_t nf, StatusWord* status, int lane) {
+  nf = max(nf, __shfl_xor_sync(0xffffffffu, nf, 16));
+  nf = max(nf, __shfl_xor_sync(0xffffffffu, nf, 8));
+  nf = max(nf, __shfl_xor_sync(0xffffffffu, nf, 4));
+  nf = max(nf, __shfl_xor_sync(0xffffffffu, nf, 2));
+  nf = max(nf, __shfl_xor_sync(0xffffffffu, nf, 1));
+  if (lane == 0 && nf >= kNonFiniteHi) atomicExch(&status->nonfinite, 1);
+}
+
+}  // namespace sqb

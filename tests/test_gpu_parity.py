@@ -1,0 +1,267 @@
+"""GPU parity tests: the CUDA path (through the C ABI, via the Python mirror of the reference
+interface) against the CPU oracle on identical seeded inputs.  Tolerances are the ones DESIGN.md
+states: R within 64*n*eps*|X|_F after sign normalisation, Gram within 5*n*eps*|X|_F^2."""
+import numpy as np
+import pytest
+
+from conftest import EPS, gaussian, normalize, r_bound
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(1000, 1), (5000, 3), (20000, 8), (4097, 5), (50000, 12), (30000, 16), (20011, 24),
+          (20000, 32), (9000, 40), (8000, 56), (10000, 64), (64, 64), (130, 7)]
+
+
+@pytest.mark.parametrize("m,n", SHAPES)
+def test_tsqr_qless_host_matches_oracle(ctx, oracle, m, n):
+    x = gaussian(m, n, seed=m + n)
+    r = ctx.tsqr_qless(x)
+    best = oracle.ref or oracle.port
+    r_ref = best.tsqr_qless(x)
+    r_hh = oracle.port.reference_hhqr(x)
+    assert np.all(np.tril(r, -1) == 0.0)
+    assert np.all(np.diag(r) >= 0.0)
+    assert np.linalg.norm(r - r_ref) <= r_bound(x)
+    assert np.linalg.norm(r - r_hh) <= r_bound(x)
+
+
+@pytest.mark.parametrize("k,b", [(1, 64), (2, 24), (13, 48), (64, 16), (7, 33), (300, 8)])
+def test_tsqr_plan_invariance(ctx, oracle, sq, k, b):
+    x = gaussian(5000, 12, seed=3)
+    r = ctx.tsqr_qless(x, sq.PanelPlan(k, b))
+    r_hh = oracle.port.reference_hhqr(x)
+    assert np.linalg.norm(r - r_hh) <= r_bound(x)
+
+
+def test_tsqr_stage1_blocks(ctx, oracle, sq):
+    x = gaussian(6000, 9, seed=11)
+    plan = sq.PanelPlan(5, 64)
+    y = ctx.tsqr_stage1(x, plan)
+    y_ref = oracle.port.tsqr_stage1(x, 5, 64)
+    assert y.shape == y_ref.shape == (45, 9)
+    for blk in range(5):
+        a = normalize(y[blk * 9:(blk + 1) * 9])
+        b_ = normalize(y_ref[blk * 9:(blk + 1) * 9])
+        lo, hi = plan.block_begin(6000, blk), plan.block_end(6000, blk)
+        assert np.linalg.norm(a - b_) <= r_bound(x[lo:hi])
+
+
+def test_block_qless_qr(ctx, oracle):
+    x = gaussian(3000, 10, seed=5)
+    r = normalize(ctx.block_qless_qr(x, 128))
+    r_ref = normalize(oracle.port.block_qless_qr(x, 128))
+    assert np.linalg.norm(r - r_ref) <= r_bound(x)
+
+
+def test_zero_column_gives_exact_zero_row(ctx):
+    x = gaussian(600, 3, seed=1)
+    x[:, 1] = 0.0
+    r = ctx.tsqr_qless(x)
+    assert np.all(r[1, :] == 0.0)
+    assert r[0, 1] == 0.0
+
+
+def test_spec_examples(ctx):
+    r = ctx.tsqr_qless(np.array([[1.0, 1.0], [0.0, 1.0], [0.0, 0.0]]))
+    assert np.allclose(r, [[1.0, 1.0], [0.0, 1.0]], atol=1e-15)
+    r = ctx.tsqr_qless(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    assert np.allclose(r, np.eye(2), atol=1e-15)
+    c = ctx.tsmttsm(np.ones((4, 2)))
+    assert np.array_equal(c, [[4.0, 4.0], [4.0, 4.0]])
+    r = ctx.cholesky(np.array([[4.0, 2.0], [2.0, 5.0]]))
+    assert np.allclose(r, [[2.0, 1.0], [0.0, 2.0]], atol=1e-15)
+    r = ctx.cholqr2(np.array([[2.0, 0.0], [0.0, 3.0], [0.0, 0.0]]))
+    assert np.allclose(r, np.diag([2.0, 3.0]), atol=1e-14)
+    vals, vecs = ctx.eigh_small(np.array([[2.0, 1.0], [1.0, 2.0]]))
+    assert np.allclose(vals, [3.0, 1.0], atol=1e-15)
+    assert np.allclose(np.abs(vecs), np.full((2, 2), 1 / np.sqrt(2)), atol=1e-15)
+    xs, res = ctx.solve_lstsq(np.ones((3, 1)), np.array([1.0, 2.0, 3.0]))
+    assert np.allclose(xs, [2.0], atol=1e-15) and abs(res - np.sqrt(2.0)) < 1e-14
+
+
+def test_errors(ctx, sq):
+    with pytest.raises(sq.ArgumentError):
+        ctx.tsqr_qless(gaussian(200, 65))
+    with pytest.raises(sq.DimensionError):
+        ctx.tsqr_qless(gaussian(1, 3))
+    x = gaussian(5000, 6)
+    x[4321, 2] = np.nan
+    with pytest.raises(sq.ArgumentError):
+        ctx.tsqr_qless(x)
+    x[4321, 2] = np.inf
+    with pytest.raises(sq.ArgumentError):
+        ctx.cholqr2(x)
+    with pytest.raises(sq.ArgumentError):
+        ctx.tsmttsm(x)
+    with pytest.raises(sq.BreakdownError) as ei:
+        ctx.cholesky(np.array([[1.0, 1.0], [1.0, 1.0]]))
+    assert ei.value.pivot_index == 1
+    with pytest.raises(sq.SingularFactorError) as ei:
+        ctx.tsmRttsmR(gaussian(100, 3), np.array([[1.0, 2.0, 3.0], [0.0, 0.0, 1.0], [0.0, 0.0, 2.0]]))
+    assert ei.value.diagonal_index == 1
+    with pytest.raises(sq.ZeroMatrixError):
+        ctx.svqb2(np.zeros((50, 4)))
+    # the context stays usable after an error
+    r = ctx.tsqr_qless(gaussian(300, 4, seed=2))
+    assert np.all(np.isfinite(r))
+
+
+@pytest.mark.parametrize("m,n", [(3000, 1), (7001, 4), (20000, 8), (12000, 16), (9000, 24),
+                                 (10000, 32), (6000, 48), (5000, 64)])
+def test_gram_kernels(ctx, oracle, m, n):
+    x = gaussian(m, n, seed=7 * n)
+    xn2 = np.linalg.norm(x) ** 2
+    c = ctx.tsmttsm(x)
+    c_ref = oracle.port.tsmttsm(x)
+    assert np.array_equal(c, c.T)
+    assert np.linalg.norm(c - c_ref) <= 5 * n * EPS * xn2
+    r1 = np.linalg.cholesky(c_ref).T.copy(order="F")
+    c2 = ctx.tsmRttsmR(x, r1)
+    c2_ref = oracle.port.tsmRttsmR(x, r1)
+    assert np.linalg.norm(c2 - c2_ref) <= 50 * n * EPS * n
+    bm = gaussian(n, n, seed=99) / np.sqrt(m)
+    c3 = ctx.tsmmttsmm(x, bm)
+    c3_ref = oracle.port.tsmmttsmm(x, bm)
+    assert np.linalg.norm(c3 - c3_ref) <= 5 * n * EPS * np.linalg.norm(x @ bm) ** 2 + 1e-300
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 8, 17, 32, 64])
+def test_cholesky_and_eigh(ctx, oracle, n):
+    a = gaussian(4 * n + 3, n, seed=n)
+    c = np.asfortranarray(a.T @ a)
+    r = ctx.cholesky(c)
+    r_ref = oracle.port.cholesky(c)
+    assert np.all(np.tril(r, -1) == 0.0)
+    assert np.linalg.norm(r - r_ref) <= 50 * n * EPS * np.linalg.norm(r_ref) * np.linalg.cond(c) ** 0.5
+    vals, vecs = ctx.eigh_small(c)
+    vals_ref, _ = oracle.port.eigh_small(c)
+    assert np.all(np.diff(vals) <= 0.0)
+    assert np.linalg.norm(vals - vals_ref) <= 50 * n * EPS * np.linalg.norm(c)
+    assert np.linalg.norm(vecs.T @ vecs - np.eye(n)) <= 50 * n * EPS
+    assert np.linalg.norm(c @ vecs - vecs * vals) <= 50 * n * EPS * np.linalg.norm(c)
+
+
+@pytest.mark.parametrize("m,n", [(4000, 3), (20000, 8), (15000, 16), (12000, 32), (9000, 64)])
+def test_cholqr2_and_svqb2(ctx, oracle, m, n):
+    x = gaussian(m, n, seed=m)
+    r = ctx.cholqr2(x)
+    r_ref = oracle.port.cholqr2(x)
+    assert np.all(np.diag(r) > 0.0)
+    assert np.linalg.norm(r - r_ref) <= r_bound(x)
+    tr, z, sg, rank = ctx.svqb2(x)
+    tr_ref, z_ref, sg_ref, rank_ref = oracle.port.svqb2(x)
+    assert rank == rank_ref == n
+    assert np.linalg.norm(sg - sg_ref) <= 50 * n * EPS * sg_ref[0]
+    c = x.T @ x
+    assert np.linalg.norm(tr.T @ c @ tr - np.eye(n)) <= 1e-12
+    assert np.linalg.norm(z @ tr - np.eye(n)) <= 1e-12
+    assert np.linalg.norm(z.T @ z - c) <= 100 * n * EPS * np.linalg.norm(c)
+
+
+def test_svqb_pass(ctx, oracle):
+    a = gaussian(300, 12, seed=8)
+    c = np.asfortranarray(a.T @ a)
+    b, z, sg, rank = ctx.svqb_pass(c)
+    b_ref, z_ref, sg_ref, rank_ref = oracle.port.svqb_pass(c)
+    assert rank == rank_ref == 12
+    assert np.linalg.norm(sg - sg_ref) <= 1e-13 * sg_ref[0]
+    assert np.linalg.norm(b.T @ c @ b - np.eye(12)) <= 1e-12
+    assert np.linalg.norm(z @ b - np.eye(12)) <= 1e-12
+    # columns agree with the reference's up to sign (well separated spectrum)
+    for j in range(12):
+        s = np.sign(b[:, j] @ b_ref[:, j])
+        assert np.linalg.norm(b[:, j] * s - b_ref[:, j]) <= 1e-9 * np.linalg.norm(b_ref[:, j])
+
+
+def test_svqb2_truncates_rank_deficient(ctx, oracle):
+    x = gaussian(5000, 6, seed=4)
+    x[:, 5] = x[:, 0] + x[:, 1]
+    tr, z, sg, rank = ctx.svqb2(x)
+    _, _, _, rank_ref = oracle.port.svqb2(x)
+    assert rank == rank_ref == 5
+    assert np.all(tr[:, 5] == 0.0) and np.all(z[5, :] == 0.0)
+
+
+@pytest.mark.parametrize("method", ["tsqr", "cholqr2", "svqb2"])
+@pytest.mark.parametrize("m,n", [(5000, 4), (20000, 15), (9000, 31)])
+def test_solve_lstsq(ctx, oracle, method, m, n):
+    a = gaussian(m, n, seed=n)
+    rhs = a @ np.arange(1, n + 1, dtype=np.float64) + 0.01 * gaussian(m, 1, seed=77)[:, 0]
+    xs, res = ctx.solve_lstsq(a, rhs, method)
+    xs_ref, res_ref = oracle.port.solve_lstsq(a, rhs, method)
+    assert np.linalg.norm(xs - xs_ref) <= 1e-10 * np.linalg.norm(xs_ref)
+    assert abs(res - res_ref) <= 1e-10 * res_ref
+
+
+def test_lstsq_rank_deficient(ctx, sq):
+    a = gaussian(400, 3, seed=1)
+    a[:, 2] = 0.0
+    with pytest.raises(sq.RankDeficiencyError) as ei:
+        ctx.solve_lstsq(a, np.ones(400))
+    assert ei.value.diagonal_index == 2
+
+
+def test_reconstruct_q(ctx, oracle):
+    x = gaussian(7000, 10, seed=6)
+    r = ctx.tsqr_qless(x)
+    q = ctx.reconstruct_q(x, r)
+    q_ref = oracle.port.reconstruct_q(x, r)
+    assert np.linalg.norm(q - q_ref) <= 1e-13 * np.linalg.norm(q_ref)
+    assert np.linalg.norm(q.T @ q - np.eye(10)) <= 1e-13
+
+
+@pytest.mark.parametrize("n,method", [(8, "tsqr"), (32, "tsqr"), (16, "cholqr2"), (8, "svqb2")])
+def test_device_pointer_path(ctx, oracle, n, method):
+    import torch
+    m = 200_000
+    x = ctx.fill_gaussian(m, n, seed=1234)
+    ctx.use_torch_stream()
+    xh = np.asfortranarray(x.cpu().numpy())
+    x_or = oracle.gaussian(m, n, 1234)
+    assert np.max(np.abs(xh - x_or)) <= 1e-13  # same stream, libm vs CUDA log/cos differ by ulps
+    if method == "tsqr":
+        r = ctx.tsqr_qless(x)
+        ctx.synchronize()
+        assert np.linalg.norm(r.cpu().numpy() - oracle.port.reference_hhqr(xh)) <= r_bound(xh)
+    elif method == "cholqr2":
+        r = ctx.cholqr2(x)
+        ctx.synchronize()
+        assert np.linalg.norm(r.cpu().numpy() - oracle.port.reference_hhqr(xh)) <= r_bound(xh)
+    else:
+        tr, z, sg, rank = ctx.svqb2(x)
+        ctx.synchronize()
+        assert int(rank.item()) == n
+        c = xh.T @ xh
+        tr = tr.cpu().numpy()
+        assert np.linalg.norm(tr.T @ c @ tr - np.eye(n)) <= 1e-12
+
+
+def test_generate_matches_reference_generator(ctx, oracle):
+    x = ctx.generate(5000, 12, 1e3, seed=42)
+    ctx.synchronize()
+    xh = x.cpu().numpy()
+    x_ref = oracle.port.generate(5000, 12, 1e3, 42)
+    assert np.max(np.abs(xh - x_ref)) <= 1e-14
+    s = np.linalg.svd(xh, compute_uv=False)
+    assert abs(s[0] / s[-1] - 1e3) <= 1e-6 * 1e3
+
+
+@pytest.mark.parametrize("kappa", [1e2, 1e6, 1e10])
+def test_ill_conditioned_stability(ctx, oracle, sq, kappa):
+    """BASELINE config 3 at reduced m: TSQR keeps R parity at every kappa; CholQR2 breaks down
+    where the reference does."""
+    x = oracle.port.generate(20000, 32, kappa, 42)
+    r = ctx.tsqr_qless(x)
+    r_hh = oracle.port.reference_hhqr(x)
+    assert np.linalg.norm(r - r_hh) <= r_bound(x)
+    ref_fails = False
+    try:
+        r_c_ref = oracle.port.cholqr2(x)
+    except oracle.OracleError as e:
+        ref_fails = e.kind == "BreakdownError"
+    if ref_fails:
+        with pytest.raises(sq.BreakdownError):
+            ctx.cholqr2(x)
+    else:
+        r_c = ctx.cholqr2(x)
+        assert np.linalg.norm(r_c - r_c_ref) <= 64 * 32 * EPS * np.linalg.norm(x) * max(1.0, kappa * 1e-4)
