@@ -50,8 +50,10 @@ typedef struct sqb_context sqb_context;
  * are allocated per call (src/tsqr.cpp:142, src/gram.cpp:44-47).                           */
 int sqb_create(sqb_context** ctx, int device);
 int sqb_destroy(sqb_context* ctx);
-/* Use a caller-owned cudaStream_t instead of the context's own.                            */
+/* Use a caller-owned cudaStream_t instead of the context's own (NULL = the CUDA default
+ * stream); sqb_use_own_stream switches back.                                               */
 int sqb_set_stream(sqb_context* ctx, void* cuda_stream);
+int sqb_use_own_stream(sqb_context* ctx);
 void* sqb_get_stream(sqb_context* ctx);
 /* Synchronise the stream and return the first error recorded since the last sync (0 = ok). */
 int sqb_sync(sqb_context* ctx);

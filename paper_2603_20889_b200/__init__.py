@@ -117,7 +117,7 @@ class PanelPlan:
 
 # ---- library loading ---------------------------------------------------------------------------
 ABI_SYMBOLS = [
-    "sqb_create", "sqb_destroy", "sqb_set_stream", "sqb_get_stream", "sqb_sync",
+    "sqb_create", "sqb_destroy", "sqb_set_stream", "sqb_use_own_stream", "sqb_get_stream", "sqb_sync",
     "sqb_last_error_index", "sqb_status_string", "sqb_device_sm_count", "sqb_launch_count",
     "sqb_default_tsqr_plan", "sqb_default_gram_plan",
     "sqb_tsqr_qless_dev", "sqb_tsqr_stage1_dev", "sqb_block_qless_qr_dev", "sqb_tsmttsm_dev",
@@ -238,7 +238,11 @@ class Context:
         return int(self.lib.sqb_launch_count(self.handle))
 
     def set_stream(self, cuda_stream_ptr):
-        self._check(self.lib.sqb_set_stream(self.handle, C.c_void_p(cuda_stream_ptr)), "set_stream")
+        """Enqueue on a caller-owned cudaStream_t (0 / None = the CUDA default stream)."""
+        self._check(self.lib.sqb_set_stream(self.handle, C.c_void_p(cuda_stream_ptr or None)), "set_stream")
+
+    def use_own_stream(self):
+        self._check(self.lib.sqb_use_own_stream(self.handle), "use_own_stream")
 
     def use_torch_stream(self):
         import torch

@@ -297,7 +297,7 @@ NcclApi& nccl() {
 }
 
 int allreduce_square(sqb_context* ctx, double* d, int n) {
-  if (ctx->world <= 1) return SQB_OK;
+  if (ctx->world <= 1 && !ctx->nccl_comm) return SQB_OK;  // an attached 1-rank communicator is used
   NcclApi& api = nccl();
   if (!api.ok || !ctx->nccl_comm) return SQB_E_NCCL;
   const int rc = api.AllReduce(d, d, static_cast<size_t>(n) * n, kNcclFloat64, kNcclSum,
@@ -320,7 +320,7 @@ __global__ void pack_stack_kernel(const double* __restrict__ gathered, int world
 
 // Local triangle -> all-gather -> redundant final combine on every rank (stage 2 with k = world).
 int tsqr_sharded_view(sqb_context* ctx, const MatView& v, long long m_local, int n, double* d_r) {
-  if (ctx->world <= 1) return tsqr_view(ctx, v, m_local, n, 0, 0, d_r, true);
+  if (ctx->world <= 1 && !ctx->nccl_comm) return tsqr_view(ctx, v, m_local, n, 0, 0, d_r, true);
   NcclApi& api = nccl();
   if (!api.ok || !ctx->nccl_comm) return SQB_E_NCCL;
   Small s;
@@ -401,8 +401,15 @@ int sqb_destroy(sqb_context* ctx) {
 
 int sqb_set_stream(sqb_context* ctx, void* cuda_stream) {
   SQB_TRY(enter(ctx));
-  ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own_stream_handle;
-  ctx->own_stream = cuda_stream == nullptr;
+  ctx->stream = static_cast<cudaStream_t>(cuda_stream);  // NULL is the CUDA default stream
+  ctx->own_stream = false;
+  return SQB_OK;
+}
+
+int sqb_use_own_stream(sqb_context* ctx) {
+  SQB_TRY(enter(ctx));
+  ctx->stream = ctx->own_stream_handle;
+  ctx->own_stream = true;
   return SQB_OK;
 }
 
