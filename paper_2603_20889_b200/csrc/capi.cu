@@ -60,7 +60,7 @@ Plan make_plan(long long m, long long k, long long b) {
 // B200 default for the Householder stream: one CTA per SM (the kernel owns the whole shared
 // memory), b = the warp panel height; fewer CTAs when there is not even one panel per warp.
 Plan tsqr_plan(const sqb_context* ctx, long long m, int n, long long k, long long b) {
-  const long long P = tsqr_warp_panel_rows(n), NW = tsqr_warp_warps(n);
+  const long long P = tsqr_panel_rows(n), NW = tsqr_warps(n);
   if (b <= 0) b = P;
   if (k <= 0) k = std::max<long long>(1, std::min<long long>(ctx->sm_count, m / (P * NW)));
   return make_plan(m, k, b);
@@ -95,7 +95,7 @@ int launch_tsqr(sqb_context* ctx, const MatView& v, long long m, int n, const Pl
   prm.finalize = finalize ? 1 : 0;
   prm.check_finite = check ? 1 : 0;
   prm.status = ctx->d_status;
-  SQB_CUDA(launch_tsqr_warp(prm, p.k, ctx->stream));
+  SQB_CUDA(launch_tsqr_any(prm, p.k, ctx->stream));
   ctx->launches++;
   return SQB_OK;
 }
@@ -104,7 +104,7 @@ int launch_tsqr(sqb_context* ctx, const MatView& v, long long m, int n, const Pl
 // triangle: the reference's stage 2 (tsqr.cpp:193-195), as a short tree of the same kernel.
 int reduce_stack(sqb_context* ctx, double* stack, long long rows, long long ld, int n,
                  double* scratch, double* d_r, bool finalize) {
-  const long long P = tsqr_warp_panel_rows(n), NW = tsqr_warp_warps(n);
+  const long long P = tsqr_panel_rows(n), NW = tsqr_warps(n);
   double* cur = stack;
   double* nxt = scratch;
   while (true) {
@@ -152,7 +152,7 @@ int gram_view(sqb_context* ctx, const MatView& v, long long m, int n, int op, co
   const Plan p = gram_plan(ctx, m, n, op, k, b);
   SQB_TRY(grow(&ctx->work, &ctx->work_doubles, static_cast<size_t>(p.k) * n * n));
   SQB_TRY(launch_gram_blocks(ctx, v, m, n, op, factor, p, ctx->work, check));
-  SQB_CUDA(launch_gram_reduce(ctx->work, p.k, n, d_c, ctx->stream));
+  SQB_CUDA(launch_gram_reduce(ctx->work, p.k, n, d_c, check ? 1 : 0, ctx->d_status, ctx->stream));
   ctx->launches++;
   return SQB_OK;
 }
@@ -485,7 +485,7 @@ int sqb_block_qless_qr_dev(sqb_context* ctx, const double* d_x, int64_t m, int64
                            int64_t panel_rows, double* d_r) {
   SQB_TRY(enter(ctx));
   if (n < 1 || n > 64 || ld < m || m < 0) return SQB_E_ARGUMENT;
-  const int64_t b = panel_rows > 0 ? panel_rows : tsqr_warp_panel_rows(static_cast<int>(n));
+  const int64_t b = panel_rows > 0 ? panel_rows : tsqr_panel_rows(static_cast<int>(n));
   Plan p{1, b, ceil_div(std::max<int64_t>(m, 1), b) * b};
   return launch_tsqr(ctx, plain_view(d_x, ld, static_cast<int>(n)), m, static_cast<int>(n), p, d_r, n,
                      false, true);
@@ -635,7 +635,7 @@ int sqb_tsqr_qless_host(sqb_context* ctx, const double* x, int64_t m, int64_t n,
     SQB_TRY(tsqr_view(ctx, plain_view(ctx->xbuf, m, nn), m, nn, num_blocks, panel_rows, s.rr, true));
   } else {
     // default plan: every slab is factored as soon as it lands; all slab triangles are stacked
-    const long long P = tsqr_warp_panel_rows(nn), NW = tsqr_warp_warps(nn);
+    const long long P = tsqr_panel_rows(nn), NW = tsqr_warps(nn);
     long long slab_rows = static_cast<long long>(kSlabBytes / (sizeof(double) * n));
     slab_rows = std::max(P, slab_rows / P * P);
     const long long nslabs = ceil_div(m, slab_rows);

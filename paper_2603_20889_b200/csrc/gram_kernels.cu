@@ -32,7 +32,7 @@ struct GramCfg {
   static constexpr int NPAD = 8 * NB;
   static constexpr int NW = NB >= 8 ? 6 : 8;
   static constexpr int NS = OP == OP_SOLVE ? 1 : 2;
-  static constexpr int RL = WarpCfg<NB>::RL;  // OP_SOLVE: register panel, same shape as TSQR
+  static constexpr int RL = WarpCfg<NB, 0>::RL;  // OP_SOLVE: register panel, same shape as TSQR
   // streaming panel heights: P == 8 (mod 16) keeps the plain fragment pattern unpadded, P == 0
   // (mod 16) costs the transposed pattern only 4 pad rows
   static constexpr int kPlainP[8] = {120, 72, 40, 40, 24, 24, 24, 24};
@@ -112,7 +112,6 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
   double acc[NPAIR][2];
 #pragma unroll
   for (int p = 0; p < NPAIR; ++p) acc[p][0] = acc[p][1] = 0.0;
-  uint32_t nf = 0;
   uint32_t phase_bits = 0;   // bit s = parity to wait for on stage s
   uint32_t async_bits = 0;   // bit s = stage s was filled by the async engine
 
@@ -145,7 +144,6 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
           a[b] = *reinterpret_cast<const double2*>(stage + (8 * b + g) * PP + 8 * t + 2 * q);
-          nf = max(nf, max(nonfinite_bits(a[b].x), nonfinite_bits(a[b].y)));
         }
         int p = 0;
 #pragma unroll
@@ -161,7 +159,7 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
     } else if (OP == OP_SOLVE) {
       constexpr int RL = Cfg::RL;
       double w[NB][RL];
-      nf = max(nf, load_panel_regs<NB, RL, PP>(w, stage, g, q));
+      load_panel_regs<NB, RL, PP>(w, stage, g, q);
       __syncwarp();
       if (pnl + NW < npanels) issue(pnl + NW, s);
       // W <- W R^-1, column by column (kernels_scalar.cpp:19-32 order: subtract earlier columns
@@ -169,6 +167,7 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
 #pragma unroll
       for (int bc = 0; bc < NB; ++bc) {
         const int cols_here = min(8, n - 8 * bc);
+#pragma unroll 1
         for (int gc = 0; gc < cols_here; ++gc) {
           const int c = 8 * bc + gc;
           if (g == gc) {
@@ -214,7 +213,6 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
         for (int b = 0; b < NB; ++b) y[b][0] = y[b][1] = 0.0;
         for (int kc = 0; kc < kchunks; ++kc) {
           const double bf = stage[(4 * kc + q) * PP + 8 * t + g];
-          nf = max(nf, nonfinite_bits(bf));
 #pragma unroll
           for (int b = 0; b < NB; ++b) {
             const double af = fac[(4 * kc + q) + (8 * b + g) * FP];
@@ -234,8 +232,6 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
       if (pnl + static_cast<long long>(NS) * NW < npanels) issue(pnl + static_cast<long long>(NS) * NW, s);
     }
   }
-
-  if (prm.check_finite) flag_nonfinite(nf, prm.status, lane);
 
   // ---- CTA reduction in fixed warp order, then the block's upper-triangle partial -------------
   for (int wi = 0; wi < NW; ++wi) {
@@ -262,7 +258,8 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
 
 // Sum the per-block partials in ascending block order over the upper triangle and mirror
 // (reference gram.cpp:81-92).
-__global__ void gram_reduce_kernel(const double* partial, long long num_blocks, int n, double* c) {
+__global__ void gram_reduce_kernel(const double* partial, long long num_blocks, int n, double* c,
+                                   int check_finite, StatusWord* status) {
   for (int idx = threadIdx.x + blockIdx.x * blockDim.x; idx < n * n; idx += blockDim.x * gridDim.x) {
     const int i = idx % n, j = idx / n;
     if (i > j) continue;
@@ -270,6 +267,7 @@ __global__ void gram_reduce_kernel(const double* partial, long long num_blocks, 
     for (long long b = 0; b < num_blocks; ++b) s += partial[b * static_cast<long long>(n) * n + idx];
     c[i + j * n] = s;
     c[j + i * n] = s;
+    if (check_finite && is_nonfinite(s)) atomicExch(&status->nonfinite, 1);
   }
 }
 
@@ -314,8 +312,9 @@ cudaError_t launch_gram(const GramParams& prm, int op, long long num_blocks, cud
 }
 
 cudaError_t launch_gram_reduce(const double* partial, long long num_blocks, int n, double* c,
-                               cudaStream_t stream) {
-  gram_reduce_kernel<<<(n * n + 255) / 256, 256, 0, stream>>>(partial, num_blocks, n, c);
+                               int check_finite, StatusWord* status, cudaStream_t stream) {
+  gram_reduce_kernel<<<(n * n + 255) / 256, 256, 0, stream>>>(partial, num_blocks, n, c, check_finite,
+                                                              status);
   return cudaGetLastError();
 }
 

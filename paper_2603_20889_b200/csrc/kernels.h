@@ -23,6 +23,26 @@ cudaError_t launch_tsqr_warp(const TsqrParams& prm, long long num_blocks, cudaSt
 int tsqr_warp_panel_rows(int n);
 int tsqr_warp_warps(int n);
 
+// ---- tsqr_thread_kernels.cu (n <= 16: every thread is a leaf of the reduction tree) --------
+constexpr int kThreadTsqrMaxN = 16;
+cudaError_t launch_tsqr_thread(const TsqrParams& prm, long long num_blocks, cudaStream_t stream);
+int tsqr_thread_chunk_rows(int n);
+int tsqr_thread_warps(int n);
+
+// Kernel selection by column count (SQB_TSQR_THREAD_MAXN overrides the crossover for tuning).
+int tsqr_thread_max_n();
+inline bool tsqr_uses_thread_kernel(int n) { return n <= tsqr_thread_max_n(); }
+inline cudaError_t launch_tsqr_any(const TsqrParams& prm, long long num_blocks, cudaStream_t stream) {
+  return tsqr_uses_thread_kernel(prm.n) ? launch_tsqr_thread(prm, num_blocks, stream)
+                                        : launch_tsqr_warp(prm, num_blocks, stream);
+}
+inline int tsqr_panel_rows(int n) {
+  return tsqr_uses_thread_kernel(n) ? tsqr_thread_chunk_rows(n) : tsqr_warp_panel_rows(n);
+}
+inline int tsqr_warps(int n) {
+  return tsqr_uses_thread_kernel(n) ? tsqr_thread_warps(n) : tsqr_warp_warps(n);
+}
+
 // ---- gram_kernels.cu ---------------------------------------------------------------------
 enum { OP_PLAIN = 0, OP_SOLVE = 1, OP_MULTIPLY = 2 };
 struct GramParams {
@@ -37,7 +57,7 @@ struct GramParams {
 };
 cudaError_t launch_gram(const GramParams& prm, int op, long long num_blocks, cudaStream_t stream);
 cudaError_t launch_gram_reduce(const double* partial, long long num_blocks, int n, double* c,
-                               cudaStream_t stream);
+                               int check_finite, StatusWord* status, cudaStream_t stream);
 int gram_panel_rows(int n, int op);
 int gram_warps(int n);
 

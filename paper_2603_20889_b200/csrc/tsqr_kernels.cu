@@ -9,15 +9,17 @@
 //                           The same kernel, launched on Y, is the inter-CTA combine
 //                           (reference stage 2, tsqr.cpp:193-195) and applies sign_normalize
 //                           (reference src/types.cpp:8-14) when `finalize` is set.
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace sqb {
 
-template <int NB>
-__global__ void __launch_bounds__(WarpLayout<NB>::NW * kWarp, 1)
+template <int NB, int VAR>
+__global__ void __launch_bounds__(WarpLayout<NB, VAR>::NW * kWarp, 1)
     tsqr_warp_kernel(const TsqrParams prm) {
-  using L = WarpLayout<NB>;
-  constexpr int RL = L::RL, P = L::P, PP = L::PP, NW = L::NW;
+  using L = WarpLayout<NB, VAR>;
+  constexpr int RL = L::RL, P = L::P, PP = L::PP, NW = L::NW, NPAD = L::NPAD;
   extern __shared__ __align__(128) double smem[];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -44,7 +46,6 @@ __global__ void __launch_bounds__(WarpLayout<NB>::NW * kWarp, 1)
 
   const bool aligned = view_bulk_aligned(prm.x, n, begin);
   uint32_t phase = 0;
-  uint32_t nf = 0;
   auto issue = [&](long long pnl) -> bool {
     return issue_panel<P, PP>(prm.x, n, begin + pnl * P, end, aligned, stage, bar, lane);
   };
@@ -58,13 +59,11 @@ __global__ void __launch_bounds__(WarpLayout<NB>::NW * kWarp, 1)
       mbar_wait(bar, phase);
       phase ^= 1;
     }
-    nf = max(nf, load_panel_regs<NB, RL, PP>(w, stage, g, q));
+    load_panel_regs<NB, RL, PP>(w, stage, g, q);
     __syncwarp();
     if (pnl + NW < npanels) async = issue(pnl + NW);
     factor_panel<NB, RL>(w, tri, vbuf, n, lane);
   }
-
-  if (prm.check_finite) flag_nonfinite(nf, prm.status, lane);
 
   // ---- intra-CTA combine: warp 0 folds the other warps' triangles (as dense row panels) ----
   __syncthreads();
@@ -83,7 +82,7 @@ __global__ void __launch_bounds__(WarpLayout<NB>::NW * kWarp, 1)
           const int row = static_cast<int>(vr % n);
           if (row <= col)
             val = smem[static_cast<size_t>(src) * L::kWarpDoubles + L::kStageDoubles +
-                       tri_index(row, col)];
+                       row_base(row, NPAD) + col];
         }
         w[b][i] = val;
       }
@@ -93,74 +92,101 @@ __global__ void __launch_bounds__(WarpLayout<NB>::NW * kWarp, 1)
 
   // ---- write the CTA's triangle: rows [blk*n, blk*n+n) of Y, full square with zeros below ----
   double* dst = prm.y + blk * n;
+  bool bad = false;
   for (int idx = lane; idx < n * n; idx += kWarp) {
     const int i = idx % n, j = idx / n;
     double val = 0.0;
     if (i <= j) {
-      val = tri[tri_index(i, j)];
-      if (prm.finalize && tri[tri_index(i, i)] < 0.0) val = -val;
+      val = tri[row_base(i, NPAD) + j];
+      bad = bad || is_nonfinite(val);
+      if (prm.finalize && tri[row_base(i, NPAD) + i] < 0.0) val = -val;
     }
     dst[i + j * prm.ldy] = val;
   }
+  if (prm.check_finite && bad) atomicExch(&prm.status->nonfinite, 1);
 }
 
 // ---------------------------------------------------------------------------------------------
 // host-side launcher
 // ---------------------------------------------------------------------------------------------
-template <int NB>
+template <int NB, int VAR>
 static cudaError_t launch_nb(const TsqrParams& prm, long long num_blocks, cudaStream_t stream) {
-  using L = WarpLayout<NB>;
+  using L = WarpLayout<NB, VAR>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(tsqr_warp_kernel<NB>,
+    cudaError_t e = cudaFuncSetAttribute(tsqr_warp_kernel<NB, VAR>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(L::kSmemBytes));
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  tsqr_warp_kernel<NB><<<static_cast<unsigned>(num_blocks), L::NW * kWarp, L::kSmemBytes, stream>>>(prm);
+  tsqr_warp_kernel<NB, VAR>
+      <<<static_cast<unsigned>(num_blocks), L::NW * kWarp, L::kSmemBytes, stream>>>(prm);
   return cudaGetLastError();
 }
 
+// Which tuning variant runs for a given column-block count (see WarpCfg).  SQB_TSQR_VARIANT
+// (0/1) overrides the table - used by the tuning sweeps in tools/.
+static int tsqr_variant(int nb) {
+  static int forced = [] {
+    const char* e = getenv("SQB_TSQR_VARIANT");
+    return e ? atoi(e) : -1;
+  }();
+  if (forced == 0 || forced == 1) return forced;
+  static const int table[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  return table[nb];
+}
+
+#define SQB_NB_SWITCH(EXPR0, EXPR1)                    \
+  switch (nb) {                                        \
+    case 1: return var ? EXPR1(1) : EXPR0(1);          \
+    case 2: return var ? EXPR1(2) : EXPR0(2);          \
+    case 3: return var ? EXPR1(3) : EXPR0(3);          \
+    case 4: return var ? EXPR1(4) : EXPR0(4);          \
+    case 5: return var ? EXPR1(5) : EXPR0(5);          \
+    case 6: return var ? EXPR1(6) : EXPR0(6);          \
+    case 7: return var ? EXPR1(7) : EXPR0(7);          \
+    default: return var ? EXPR1(8) : EXPR0(8);         \
+  }
+
 cudaError_t launch_tsqr_warp(const TsqrParams& prm, long long num_blocks, cudaStream_t stream) {
   const int nb = (prm.n + 7) / 8;
-  switch (nb) {
-    case 1: return launch_nb<1>(prm, num_blocks, stream);
-    case 2: return launch_nb<2>(prm, num_blocks, stream);
-    case 3: return launch_nb<3>(prm, num_blocks, stream);
-    case 4: return launch_nb<4>(prm, num_blocks, stream);
-    case 5: return launch_nb<5>(prm, num_blocks, stream);
-    case 6: return launch_nb<6>(prm, num_blocks, stream);
-    case 7: return launch_nb<7>(prm, num_blocks, stream);
-    case 8: return launch_nb<8>(prm, num_blocks, stream);
-    default: return cudaErrorInvalidValue;
-  }
+  if (nb < 1 || nb > 8) return cudaErrorInvalidValue;
+  const int var = tsqr_variant(nb);
+#define L0(NBV) launch_nb<NBV, 0>(prm, num_blocks, stream)
+#define L1(NBV) launch_nb<NBV, 1>(prm, num_blocks, stream)
+  SQB_NB_SWITCH(L0, L1)
+#undef L0
+#undef L1
+}
+
+int tsqr_thread_max_n() {
+  static int v = [] {
+    const char* e = getenv("SQB_TSQR_THREAD_MAXN");
+    const int x = e ? atoi(e) : kThreadTsqrMaxN;
+    return x < 0 ? 0 : (x > kThreadTsqrMaxN ? kThreadTsqrMaxN : x);
+  }();
+  return v;
 }
 
 int tsqr_warp_warps(int n) {
-  switch ((n + 7) / 8) {
-    case 1: return WarpLayout<1>::NW;
-    case 2: return WarpLayout<2>::NW;
-    case 3: return WarpLayout<3>::NW;
-    case 4: return WarpLayout<4>::NW;
-    case 5: return WarpLayout<5>::NW;
-    case 6: return WarpLayout<6>::NW;
-    case 7: return WarpLayout<7>::NW;
-    default: return WarpLayout<8>::NW;
-  }
+  const int nb = (n + 7) / 8;
+  const int var = tsqr_variant(nb);
+#define W0(NBV) WarpLayout<NBV, 0>::NW
+#define W1(NBV) WarpLayout<NBV, 1>::NW
+  SQB_NB_SWITCH(W0, W1)
+#undef W0
+#undef W1
 }
 
 int tsqr_warp_panel_rows(int n) {
-  switch ((n + 7) / 8) {
-    case 1: return WarpLayout<1>::P;
-    case 2: return WarpLayout<2>::P;
-    case 3: return WarpLayout<3>::P;
-    case 4: return WarpLayout<4>::P;
-    case 5: return WarpLayout<5>::P;
-    case 6: return WarpLayout<6>::P;
-    case 7: return WarpLayout<7>::P;
-    default: return WarpLayout<8>::P;
-  }
+  const int nb = (n + 7) / 8;
+  const int var = tsqr_variant(nb);
+#define P0(NBV) WarpLayout<NBV, 0>::P
+#define P1(NBV) WarpLayout<NBV, 1>::P
+  SQB_NB_SWITCH(P0, P1)
+#undef P0
+#undef P1
 }
 
 }  // namespace sqb

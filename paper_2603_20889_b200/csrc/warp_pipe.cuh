@@ -43,10 +43,13 @@ __device__ __forceinline__ bool issue_panel(const MatView& x, int n, long long r
                                             bool aligned, double* stage, uint64_t* bar, int lane) {
   const long long left = end - r0;
   if (aligned && left >= P) {
-    if (lane == 0) {
+    // lane 0 arms the barrier, then lane j issues the copy of column j: one UBLKCP per lane
+    // instead of an n-iteration loop on a single lane.
+    if (lane == 0) mbar_expect_tx(bar, static_cast<uint32_t>(n * P * sizeof(double)));
+    __syncwarp();
+    for (int j = lane; j < n; j += kWarp) {
       fence_async_smem();
-      mbar_expect_tx(bar, static_cast<uint32_t>(n * P * sizeof(double)));
-      for (int j = 0; j < n; ++j) bulk_g2s(stage + j * PP, x.col(j) + r0, P * sizeof(double), bar);
+      bulk_g2s(stage + j * PP, x.col(j) + r0, P * sizeof(double), bar);
     }
     return true;
   }
@@ -59,15 +62,9 @@ __device__ __forceinline__ bool issue_panel(const MatView& x, int n, long long r
   return false;
 }
 
-// max over the warp of the exponent-field probe (fused non-finite validation, replaces the
-// reference's serial scans: src/types.cpp:40-48, src/gram.cpp:96-102).
-__device__ __forceinline__ void flag_nonfinite(uint32_t nf, StatusWord* status, int lane) {
-  nf = max(nf, __shfl_xor_sync(0xffffffffu, nf, 16));
-  nf = max(nf, __shfl_xor_sync(0xffffffffu, nf, 8));
-  nf = max(nf, __shfl_xor_sync(0xffffffffu, nf, 4));
-  nf = max(nf, __shfl_xor_sync(0xffffffffu, nf, 2));
-  nf = max(nf, __shfl_xor_sync(0xffffffffu, nf, 1));
-  if (lane == 0 && nf >= kNonFiniteHi) atomicExch(&status->nonfinite, 1);
-}
+// Fused non-finite validation (replaces the reference's serial scans, src/types.cpp:40-48 and
+// src/gram.cpp:96-102): an Inf/NaN anywhere in X makes the squared norm of its column - hence the
+// diagonal of R or of the Gram matrix - non-finite, so testing the n x n result is enough.
+__device__ __forceinline__ bool is_nonfinite(double x) { return nonfinite_bits(x) >= kNonFiniteHi; }
 
 }  // namespace sqb
