@@ -69,7 +69,8 @@ Plan tsqr_plan(const sqb_context* ctx, long long m, int n, long long k, long lon
 Plan gram_plan(const sqb_context* ctx, long long m, int n, int op, long long k, long long b) {
   const long long P = gram_panel_rows(n, op), NW = gram_warps(n);
   if (b <= 0) b = P;
-  if (k <= 0) k = std::max<long long>(1, std::min<long long>(ctx->sm_count, m / (P * NW)));
+  if (k <= 0)
+    k = std::max<long long>(1, std::min<long long>(ctx->sm_count * gram_ctas_per_sm(n, op), m / (P * NW)));
   return make_plan(m, k, b);
 }
 

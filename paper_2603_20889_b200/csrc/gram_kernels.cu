@@ -303,6 +303,7 @@ static cudaError_t launch_gram_op(const GramParams& prm, long long num_blocks, c
 }
 
 cudaError_t launch_gram(const GramParams& prm, int op, long long num_blocks, cudaStream_t stream) {
+  if (prm.n <= kThreadGramMaxN) return launch_gram_thread(prm, op, num_blocks, stream);
   switch (op) {
     case OP_PLAIN: return launch_gram_op<OP_PLAIN>(prm, num_blocks, stream);
     case OP_SOLVE: return launch_gram_op<OP_SOLVE>(prm, num_blocks, stream);
@@ -319,6 +320,7 @@ cudaError_t launch_gram_reduce(const double* partial, long long num_blocks, int 
 }
 
 int gram_panel_rows(int n, int op) {
+  if (n <= kThreadGramMaxN) return gram_thread_chunk_rows(n, op);
   const int nb = (n + 7) / 8;
 #define SQB_CASE(NBV)                                                                   \
   case NBV:                                                                              \
@@ -332,6 +334,11 @@ int gram_panel_rows(int n, int op) {
 #undef SQB_CASE
 }
 
-int gram_warps(int n) { return (n + 7) / 8 >= 8 ? 6 : 8; }
+int gram_warps(int n) {
+  if (n <= kThreadGramMaxN) return gram_thread_warps();
+  return (n + 7) / 8 >= 8 ? 6 : 8;
+}
+
+int gram_ctas_per_sm(int n, int op) { return n <= kThreadGramMaxN ? gram_thread_ctas_per_sm(n, op) : 1; }
 
 }  // namespace sqb

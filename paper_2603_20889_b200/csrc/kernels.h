@@ -29,18 +29,45 @@ cudaError_t launch_tsqr_thread(const TsqrParams& prm, long long num_blocks, cuda
 int tsqr_thread_chunk_rows(int n);
 int tsqr_thread_warps(int n);
 
-// Kernel selection by column count (SQB_TSQR_THREAD_MAXN overrides the crossover for tuning).
-int tsqr_thread_max_n();
-inline bool tsqr_uses_thread_kernel(int n) { return n <= tsqr_thread_max_n(); }
+// ---- tsqr_group_kernels.cu (8 < n <= 64: a group of G lanes is a leaf of the tree) ---------
+cudaError_t launch_tsqr_group(const TsqrParams& prm, long long num_blocks, cudaStream_t stream);
+int tsqr_group_chunk_rows(int n);
+int tsqr_group_warps(int n);
+
+// Kernel selection by column count (measured on B200, profiles/): thread-private up to 14 columns,
+// lane groups for 15..24 and 33..64, the warp-panel kernel for 25..32.  SQB_TSQR_KERNEL=0/1/2 forces
+// thread / group / warp-panel where the column count allows it (tuning and A/B tests only).
+int tsqr_forced_kind();
+inline int tsqr_kernel_kind(int n) {
+  const int f = tsqr_forced_kind();
+  if (f == 0 && n <= kThreadTsqrMaxN) return 0;
+  if (f == 1 && n > 8) return 1;
+  if (f == 2) return 2;
+  if (n <= 14) return 0;
+  if (n <= 24) return 1;
+  if (n <= 32) return 2;
+  return 1;
+}
 inline cudaError_t launch_tsqr_any(const TsqrParams& prm, long long num_blocks, cudaStream_t stream) {
-  return tsqr_uses_thread_kernel(prm.n) ? launch_tsqr_thread(prm, num_blocks, stream)
-                                        : launch_tsqr_warp(prm, num_blocks, stream);
+  switch (tsqr_kernel_kind(prm.n)) {
+    case 0: return launch_tsqr_thread(prm, num_blocks, stream);
+    case 1: return launch_tsqr_group(prm, num_blocks, stream);
+    default: return launch_tsqr_warp(prm, num_blocks, stream);
+  }
 }
 inline int tsqr_panel_rows(int n) {
-  return tsqr_uses_thread_kernel(n) ? tsqr_thread_chunk_rows(n) : tsqr_warp_panel_rows(n);
+  switch (tsqr_kernel_kind(n)) {
+    case 0: return tsqr_thread_chunk_rows(n);
+    case 1: return tsqr_group_chunk_rows(n);
+    default: return tsqr_warp_panel_rows(n);
+  }
 }
 inline int tsqr_warps(int n) {
-  return tsqr_uses_thread_kernel(n) ? tsqr_thread_warps(n) : tsqr_warp_warps(n);
+  switch (tsqr_kernel_kind(n)) {
+    case 0: return tsqr_thread_warps(n);
+    case 1: return tsqr_group_warps(n);
+    default: return tsqr_warp_warps(n);
+  }
 }
 
 // ---- gram_kernels.cu ---------------------------------------------------------------------
@@ -60,6 +87,15 @@ cudaError_t launch_gram_reduce(const double* partial, long long num_blocks, int 
                                int check_finite, StatusWord* status, cudaStream_t stream);
 int gram_panel_rows(int n, int op);
 int gram_warps(int n);
+int gram_ctas_per_sm(int n, int op);
+
+// ---- gram_thread_kernels.cu (n <= 8: register-resident rows and accumulators) --------------
+constexpr int kThreadGramMaxN = 8;
+cudaError_t launch_gram_thread(const GramParams& prm, int op, long long num_blocks,
+                               cudaStream_t stream);
+int gram_thread_chunk_rows(int n, int op);
+int gram_thread_warps();
+int gram_thread_ctas_per_sm(int n, int op);
 
 // ---- small_kernels.cu (n x n work, one CTA each) -------------------------------------------
 constexpr int kSmallMaxN = 128;

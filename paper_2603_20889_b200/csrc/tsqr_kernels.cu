@@ -160,11 +160,10 @@ cudaError_t launch_tsqr_warp(const TsqrParams& prm, long long num_blocks, cudaSt
 #undef L1
 }
 
-int tsqr_thread_max_n() {
+int tsqr_forced_kind() {
   static int v = [] {
-    const char* e = getenv("SQB_TSQR_THREAD_MAXN");
-    const int x = e ? atoi(e) : kThreadTsqrMaxN;
-    return x < 0 ? 0 : (x > kThreadTsqrMaxN ? kThreadTsqrMaxN : x);
+    const char* e = getenv("SQB_TSQR_KERNEL");
+    return e ? atoi(e) : -1;
   }();
   return v;
 }
