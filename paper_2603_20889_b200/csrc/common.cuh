@@ -94,34 +94,51 @@ __device__ __forceinline__ uint32_t nonfinite_bits(double x) {
 }
 constexpr uint32_t kNonFiniteHi = 0x7ff00000u;
 
-// sqrt(a) for a >= 0 built on the reciprocal-square-root unit plus one residual correction
-// (result within 1 ulp of the correctly rounded root); returns 0 for a == 0.
-__device__ __forceinline__ double sqrt_pos(double a) {
-  const double y = rsqrt(a);
-  double r = a * y;
-  const double e = fma(-r, r, a);
-  r = fma(e, 0.5 * y, r);
-  return a > 0.0 ? r : (a == 0.0 ? 0.0 : a * y);  // a*y propagates NaN/Inf
-}
-
 // Householder reflector scalars for the pencil [pivot; tail], sigma = |tail|^2, in the
 // un-normalised form  H = I - gamma * u u^T,  u = [u0; tail],  u0 = pivot - beta,
-// gamma = 1 / (beta * (beta - pivot)).  Same sign convention as the reference's
-// make_reflector (tsqr.cpp:51-71): beta = -norm when pivot > 0 else +norm; sigma == 0 gives the
-// identity (gamma = 0, beta = pivot) so a zero column keeps an exact zero diagonal.
+// gamma = 1 / (norm * (norm + |pivot|)),  norm = sqrt(pivot^2 + sigma).  Same sign convention as the
+// reference's make_reflector (tsqr.cpp:51-71): beta = -norm when pivot > 0 else +norm; sigma == 0
+// gives the identity (gamma = u0 = 0, beta = pivot) so a zero column keeps an exact zero diagonal.
+//
+// The scalar chain is the serial bottleneck of every Householder kernel here, so it is kept short:
+// Goldschmidt sqrt/rsqrt from the MUFU seed (two coupled iterations + one residual correction:
+// norm within 1 ulp) and a Newton reciprocal.  Outside [1e-290, 1e290] the IEEE sqrt/div path runs
+// (Inf/NaN propagate into R, which is how non-finite input is detected); below 1e-305 the
+// reciprocal would overflow - such a column is numerically zero and the reflector is the identity.
 struct Reflector {
   double beta, u0, gamma;
 };
 __device__ __forceinline__ Reflector make_reflector(double pivot, double sigma) {
   Reflector h;
-  const double norm = sqrt_pos(fma(pivot, pivot, sigma));
+  const double a = fma(pivot, pivot, sigma);
+  double norm, inv;
+  if (a > 1e-290 && a < 1e290) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+    double g = a * y, hh = 0.5 * y;
+    double r = fma(-g, hh, 0.5);
+    g = fma(g, r, g);
+    hh = fma(hh, r, hh);
+    r = fma(-g, hh, 0.5);
+    g = fma(g, r, g);
+    hh = fma(hh, r, hh);
+    norm = fma(fma(-g, g, a), hh, g);
+    const double d = norm * (norm + fabs(pivot));
+    double z;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(z) : "d"(d));
+    double e = fma(-d, z, 1.0);
+    z = fma(z, e, z);
+    e = fma(-d, z, 1.0);
+    inv = fma(z, e, z);
+  } else {
+    norm = sqrt(a);
+    inv = 1.0 / (norm * (norm + fabs(pivot)));
+  }
   const double beta = pivot > 0.0 ? -norm : norm;
-  const double u0 = pivot - beta;
-  const double den = beta * (-u0);
-  const bool live = sigma != 0.0;
+  const bool live = sigma != 0.0 && !(a < 1e-305);
   h.beta = live ? beta : pivot;
-  h.u0 = live ? u0 : 0.0;
-  h.gamma = live ? __drcp_rn(den) : 0.0;
+  h.u0 = live ? pivot - beta : 0.0;
+  h.gamma = live ? inv : 0.0;
   return h;
 }
 

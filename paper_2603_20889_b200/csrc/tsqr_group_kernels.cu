@@ -43,43 +43,6 @@ struct GroupCfg {
   static_assert(P % 2 == 0, "row pairs");
 };
 
-// Householder scalars (same derivation as tsqr_thread_kernels.cu: Goldschmidt sqrt from the MUFU
-// seed, Newton reciprocal; reference sign convention tsqr.cpp:51-71; sigma == 0 -> identity).
-__device__ __forceinline__ Reflector reflector_fast(double pivot, double sigma) {
-  Reflector h;
-  const double a = fma(pivot, pivot, sigma);
-  const bool regular = a > 1e-290 && a < 1e290;
-  double norm, inv;
-  if (regular) {
-    double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
-    double g = a * y, hh = 0.5 * y;
-    double r = fma(-g, hh, 0.5);
-    g = fma(g, r, g);
-    hh = fma(hh, r, hh);
-    r = fma(-g, hh, 0.5);
-    g = fma(g, r, g);
-    hh = fma(hh, r, hh);
-    norm = fma(fma(-g, g, a), hh, g);
-    const double d = norm * (norm + fabs(pivot));
-    double z;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(z) : "d"(d));
-    double e = fma(-d, z, 1.0);
-    z = fma(z, e, z);
-    e = fma(-d, z, 1.0);
-    inv = fma(z, e, z);
-  } else {
-    norm = sqrt(a);
-    inv = 1.0 / (norm * (norm + fabs(pivot)));
-  }
-  const double beta = pivot > 0.0 ? -norm : norm;
-  const bool live = sigma != 0.0;
-  h.beta = live ? beta : pivot;
-  h.u0 = live ? pivot - beta : 0.0;
-  h.gamma = live ? inv : 0.0;
-  return h;
-}
-
 // Fold the group's P x n register panel (w[slot][row], column = slot*G + g) into its triangle
 // (packed row-major, row_base() from tsqr_warp.cuh).  Lanes whose column is already finished run
 // the same instructions on values nobody reads again; only the R store is predicated.
@@ -109,7 +72,7 @@ __device__ __forceinline__ void fold_group(double (&w)[NS][P], double* tri, int 
         s0 = fma(v[i], v[i], s0);
         s1 = fma(v[i + 1], v[i + 1], s1);
       }
-      const Reflector h = reflector_fast(pivot, s0 + s1);
+      const Reflector h = make_reflector(pivot, s0 + s1);
 #pragma unroll
       for (int s = bc; s < NS; ++s) {
         double d0 = 0.0, d1 = 0.0;

@@ -40,44 +40,6 @@ struct ThreadCfg {
   static constexpr int kChunk = 32 * P;                 // rows a warp consumes per step
 };
 
-// Householder scalars with a short dependency chain: Goldschmidt sqrt/rsqrt from the MUFU seed
-// (two coupled iterations + one residual correction: norm within 1 ulp) and a Newton reciprocal.
-// Sign convention as reference make_reflector (tsqr.cpp:51-71); sigma == 0 -> identity.
-__device__ __forceinline__ Reflector reflector_fast(double pivot, double sigma) {
-  Reflector h;
-  const double a = fma(pivot, pivot, sigma);
-  const bool regular = a > 1e-290 && a < 1e290;
-  double norm, inv;
-  if (regular) {
-    double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
-    double g = a * y, hh = 0.5 * y;
-    double r = fma(-g, hh, 0.5);
-    g = fma(g, r, g);
-    hh = fma(hh, r, hh);
-    r = fma(-g, hh, 0.5);
-    g = fma(g, r, g);
-    hh = fma(hh, r, hh);
-    norm = fma(fma(-g, g, a), hh, g);
-    const double d = norm * (norm + fabs(pivot));
-    double z;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(z) : "d"(d));
-    double e = fma(-d, z, 1.0);
-    z = fma(z, e, z);
-    e = fma(-d, z, 1.0);
-    inv = fma(z, e, z);
-  } else {  // zero, tiny, huge or non-finite: IEEE path (NaN/Inf propagate into R)
-    norm = sqrt(a);
-    inv = 1.0 / (norm * (norm + fabs(pivot)));
-  }
-  const double beta = pivot > 0.0 ? -norm : norm;
-  const bool live = sigma != 0.0;
-  h.beta = live ? beta : pivot;
-  h.u0 = live ? pivot - beta : 0.0;
-  h.gamma = live ? inv : 0.0;
-  return h;
-}
-
 // Running triangle accessor: packed row-major (row c holds (c, c..N-1)); registers or an
 // interleaved shared-memory slot (element e of thread t at rs[e*T + t]).
 template <int N, bool REG, int T>
@@ -109,7 +71,7 @@ __device__ __forceinline__ void fold_rows(double (&w)[N][P], Tri<N, REG, T>& tri
       s1 = fma(w[c][i + 1], w[c][i + 1], s1);
     }
     const double pivot = tri.get(c, c);
-    const Reflector h = reflector_fast(pivot, s0 + s1);
+    const Reflector h = make_reflector(pivot, s0 + s1);
     static_for<c + 1, N>([&](auto jj) {
       constexpr int j = decltype(jj)::value;
       double d0 = 0.0, d1 = 0.0;

@@ -265,3 +265,87 @@ def test_ill_conditioned_stability(ctx, oracle, sq, kappa):
     else:
         r_c = ctx.cholqr2(x)
         assert np.linalg.norm(r_c - r_c_ref) <= 64 * 32 * EPS * np.linalg.norm(x) * max(1.0, kappa * 1e-4)
+
+
+def test_nccl_collective_path_single_rank(sq, oracle):
+    """The sharded entry points with a real (1-rank) NCCL communicator: all-gather + combine for
+    TSQR, all-reduce for the Gram methods.  More ranks need more GPUs than this box has."""
+    import torch
+    c = sq.Context(0)
+    c.use_torch_stream()
+    c.init_nccl(c.nccl_unique_id(), 0, 1)
+    m, n = 300_000, 12
+    x = c.fill_gaussian(m, n, seed=5)
+    r = c.tsqr_qless_sharded(x)
+    rc = c.cholqr2_sharded(x)
+    tr, z, sg, rank = c.svqb2_sharded(x)
+    rhs = torch.ones(m, dtype=torch.float64, device=x.device)
+    xs, res = c.solve_lstsq_sharded(x, rhs)
+    c.synchronize()
+    xh = np.asfortranarray(x.cpu().numpy())
+    r_ref = oracle.port.reference_hhqr(xh)
+    assert np.linalg.norm(r.cpu().numpy() - r_ref) <= r_bound(xh)
+    assert np.linalg.norm(rc.cpu().numpy() - r_ref) <= r_bound(xh)
+    assert int(rank.item()) == n
+    xs_ref, res_ref = oracle.port.solve_lstsq(xh, np.ones(m), "tsqr")
+    assert np.allclose(xs.cpu().numpy(), xs_ref, rtol=1e-9, atol=1e-12)
+    assert abs(float(res.item()) - res_ref) <= 1e-10 * res_ref
+    c.close()
+
+
+def test_large_m_self_consistency(ctx):
+    """Full-size style check without the oracle: R^T R of TSQR equals the independently computed
+    Gram matrix, and CholQR2's R equals TSQR's (size-independent properties)."""
+    m, n = 1 << 22, 16
+    x = ctx.fill_gaussian(m, n, seed=9)
+    ctx.use_torch_stream()
+    r = ctx.tsqr_qless(x)
+    c = ctx.tsmttsm(x)
+    rc = ctx.cholqr2(x)
+    ctx.synchronize()
+    r, c, rc = r.cpu().numpy(), c.cpu().numpy(), rc.cpu().numpy()
+    xn2 = np.trace(c)
+    assert np.linalg.norm(r.T @ r - c) <= 50 * n * EPS * xn2
+    assert np.linalg.norm(r - rc) <= 64 * n * EPS * np.sqrt(xn2)
+
+
+@pytest.mark.parametrize("n", [4, 8, 9, 12, 13, 16, 20, 31, 40, 63])
+def test_device_lstsq_with_constant_rhs(ctx, oracle, n):
+    """Regression: leaves with fewer rows than columns exhaust their rank in the first fold and then
+    see reflector norms that underflow (1e-32, 1e-64, ... ) - the reflector scalars must not
+    overflow there.  Also covers the separate-rhs device path (MatView::extra)."""
+    import torch
+    m = 20_000
+    x = ctx.fill_gaussian(m, n, seed=5)
+    ctx.use_torch_stream()
+    rhs = torch.ones(m, dtype=torch.float64, device=x.device)
+    for method in ("tsqr", "cholqr2"):
+        xs, res = ctx.solve_lstsq(x, rhs, method)
+        ctx.synchronize()
+        xh = np.asfortranarray(x.cpu().numpy())
+        xs_ref, res_ref = oracle.port.solve_lstsq(xh, np.ones(m), method)
+        assert np.allclose(xs.cpu().numpy(), xs_ref, rtol=1e-9, atol=1e-13)
+        assert abs(float(res.item()) - res_ref) <= 1e-10 * res_ref
+
+
+@pytest.mark.parametrize("kind", ["0", "1", "2"])
+def test_every_tsqr_kernel_family(kind, oracle):
+    """The three TSQR kernel families (thread / lane-group / warp-panel) on the same inputs, forced
+    through SQB_TSQR_KERNEL in a fresh process so that the measured selection table is bypassed."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import oracle, paper_2603_20889_b200 as sq\n"
+        "from conftest import gaussian, r_bound\n"
+        "ctx = sq.default_context()\n"
+        "for m, n in [(9000, 5), (9001, 11), (20000, 16), (7000, 24), (6000, 33), (5000, 64)]:\n"
+        "    x = gaussian(m, n, seed=n); x[:, n // 2] = 1.0\n"
+        "    r = ctx.tsqr_qless(x)\n"
+        "    assert np.linalg.norm(r - oracle.port.reference_hhqr(x)) <= r_bound(x), (m, n)\n"
+        "print('ok')\n" % (str(Path(__file__).resolve().parents[1]), str(Path(__file__).resolve().parent)))
+    import os
+    env = dict(os.environ, SQB_TSQR_KERNEL=kind)
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
