@@ -100,40 +100,38 @@ constexpr uint32_t kNonFiniteHi = 0x7ff00000u;
 // reference's make_reflector (tsqr.cpp:51-71): beta = -norm when pivot > 0 else +norm; sigma == 0
 // gives the identity (gamma = u0 = 0, beta = pivot) so a zero column keeps an exact zero diagonal.
 //
-// The scalar chain is the serial bottleneck of every Householder kernel here, so it is kept short:
+// The scalar chain is the serial bottleneck of every Householder kernel here, so it is short and
+// BRANCH-FREE (one basic block per fold lets ptxas overlap it with the trailing updates):
 // Goldschmidt sqrt/rsqrt from the MUFU seed (two coupled iterations + one residual correction:
-// norm within 1 ulp) and a Newton reciprocal.  Outside [1e-290, 1e290] the IEEE sqrt/div path runs
-// (Inf/NaN propagate into R, which is how non-finite input is detected); below 1e-305 the
-// reciprocal would overflow - such a column is numerically zero and the reflector is the identity.
+// norm within 1 ulp) and a Newton reciprocal.  Inf/NaN propagate through it into R, which is how
+// non-finite input is detected.  Guards: a = pivot^2 + sigma below 1e-305 (the reciprocal would
+// overflow; such a column is numerically zero) gives the identity; above 1e290 (squares about to
+// overflow - the reference's plain dot products are garbage there as well) norm is poisoned with
+// NaN so that the call reports ArgumentError instead of a silently wrong R.
 struct Reflector {
   double beta, u0, gamma;
 };
 __device__ __forceinline__ Reflector make_reflector(double pivot, double sigma) {
   Reflector h;
   const double a = fma(pivot, pivot, sigma);
-  double norm, inv;
-  if (a > 1e-290 && a < 1e290) {
-    double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
-    double g = a * y, hh = 0.5 * y;
-    double r = fma(-g, hh, 0.5);
-    g = fma(g, r, g);
-    hh = fma(hh, r, hh);
-    r = fma(-g, hh, 0.5);
-    g = fma(g, r, g);
-    hh = fma(hh, r, hh);
-    norm = fma(fma(-g, g, a), hh, g);
-    const double d = norm * (norm + fabs(pivot));
-    double z;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(z) : "d"(d));
-    double e = fma(-d, z, 1.0);
-    z = fma(z, e, z);
-    e = fma(-d, z, 1.0);
-    inv = fma(z, e, z);
-  } else {
-    norm = sqrt(a);
-    inv = 1.0 / (norm * (norm + fabs(pivot)));
-  }
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  double g = a * y, hh = 0.5 * y;
+  double r = fma(-g, hh, 0.5);
+  g = fma(g, r, g);
+  hh = fma(hh, r, hh);
+  r = fma(-g, hh, 0.5);
+  g = fma(g, r, g);
+  hh = fma(hh, r, hh);
+  double norm = fma(fma(-g, g, a), hh, g);
+  norm = a > 1e290 ? __longlong_as_double(0x7ff8000000000000ll) : norm;
+  const double d = norm * (norm + fabs(pivot));
+  double z;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(z) : "d"(d));
+  double e = fma(-d, z, 1.0);
+  z = fma(z, e, z);
+  e = fma(-d, z, 1.0);
+  const double inv = fma(z, e, z);
   const double beta = pivot > 0.0 ? -norm : norm;
   const bool live = sigma != 0.0 && !(a < 1e-305);
   h.beta = live ? beta : pivot;

@@ -145,14 +145,18 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
         for (int b = 0; b < NB; ++b) {
           a[b] = *reinterpret_cast<const double2*>(stage + (8 * b + g) * PP + 8 * t + 2 * q);
         }
+        // all pairs with the even rows, then all pairs with the odd rows: NPAIR independent MMAs
+        // between two updates of the same accumulator
         int p = 0;
 #pragma unroll
         for (int b = 0; b < NB; ++b)
 #pragma unroll
-          for (int b2 = b; b2 < NB; ++b2, ++p) {
-            dmma884(acc[p][0], acc[p][1], a[b].x, a[b2].x);
-            dmma884(acc[p][0], acc[p][1], a[b].y, a[b2].y);
-          }
+          for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], a[b].x, a[b2].x);
+        p = 0;
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+          for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], a[b].y, a[b2].y);
       }
       __syncwarp();
       if (pnl + static_cast<long long>(NS) * NW < npanels) issue(pnl + static_cast<long long>(NS) * NW, s);
@@ -198,13 +202,14 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
           __syncwarp();
         }
       }
-      int p = 0;
 #pragma unroll
-      for (int b = 0; b < NB; ++b)
+      for (int i = 0; i < RL; ++i) {
+        int p = 0;
 #pragma unroll
-        for (int b2 = b; b2 < NB; ++b2, ++p)
+        for (int b = 0; b < NB; ++b)
 #pragma unroll
-          for (int i = 0; i < RL; ++i) dmma884(acc[p][0], acc[p][1], w[b][i], w[b2][i]);
+          for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], w[b][i], w[b2][i]);
+      }
     } else {  // OP_MULTIPLY
       const int kchunks = (n + 3) / 4;
       for (int t = 0; t < P / 8; ++t) {
@@ -223,10 +228,12 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
 #pragma unroll
         for (int b = 0; b < NB; ++b)
 #pragma unroll
-          for (int b2 = b; b2 < NB; ++b2, ++p) {
-            dmma884(acc[p][0], acc[p][1], y[b][0], y[b2][0]);
-            dmma884(acc[p][0], acc[p][1], y[b][1], y[b2][1]);
-          }
+          for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], y[b][0], y[b2][0]);
+        p = 0;
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+          for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], y[b][1], y[b2][1]);
       }
       __syncwarp();
       if (pnl + static_cast<long long>(NS) * NW < npanels) issue(pnl + static_cast<long long>(NS) * NW, s);
