@@ -12,9 +12,10 @@
 // update runs on the FP64 tensor pipe: lane (g,q) of a warp holds X[row(q), 8b+g], which is at
 // the same time the A fragment (8 columns x 4 rows, transposed) and the B fragment (4 rows x 8
 // columns) of mma.m8n8k4.f64 - so  C[8b.., 8b'..] += mma(w[b], w[b'])  needs no data movement.
-//   * OP_SOLVE applies R^-1 to the register panel by column-oriented substitution, the order the
-//     reference's trsm_right_upper uses (src/kernels_scalar.cpp:19-32), broadcasting each finished
-//     column through a P-double buffer; the panel never leaves registers before the Gram MMAs.
+//   * OP_SOLVE: every lane takes one row of the staged panel into registers, applies R^-1 by
+//     column-oriented substitution (the order of the reference's trsm_right_upper,
+//     src/kernels_scalar.cpp:19-32) and puts the row back into the stage; the Gram MMAs then read
+//     the transformed panel - X R^-1 never leaves the SM.
 //   * OP_MULTIPLY forms (X B) for 8 rows at a time with DMMAs whose accumulator layout is exactly
 //     the Gram fragment layout, then feeds those accumulators straight into the Gram MMAs.
 #include "kernels.h"
@@ -31,17 +32,18 @@ template <int NB, int OP>
 struct GramCfg {
   static constexpr int NPAD = 8 * NB;
   static constexpr int NW = NB >= 8 ? 6 : 8;
-  static constexpr int NS = OP == OP_SOLVE ? 1 : 2;
-  static constexpr int RL = WarpCfg<NB, 0>::RL;  // OP_SOLVE: register panel, same shape as TSQR
+  static constexpr int NS = (OP == OP_SOLVE && NB >= 5) ? 1 : 2;
   // streaming panel heights: P == 8 (mod 16) keeps the plain fragment pattern unpadded, P == 0
   // (mod 16) costs the transposed pattern only 4 pad rows
   static constexpr int kPlainP[8] = {120, 72, 40, 40, 24, 24, 24, 24};
   static constexpr int kMultP[8] = {112, 64, 48, 32, 32, 16, 16, 16};
+  // OP_SOLVE: one lane substitutes one row, so the panel height is a multiple of 32
+  static constexpr int kSolveP[8] = {64, 64, 32, 32, 32, 32, 32, 32};
   static constexpr int P =
-      OP == OP_SOLVE ? 4 * RL : (OP == OP_PLAIN ? kPlainP[NB - 1] : kMultP[NB - 1]);
+      OP == OP_SOLVE ? kSolveP[NB - 1] : (OP == OP_PLAIN ? kPlainP[NB - 1] : kMultP[NB - 1]);
   static constexpr int PP = stage_pitch(P, OP == OP_MULTIPLY ? 4 : 8);
   static constexpr int kStageDoubles = NPAD * PP;
-  static constexpr int kVbuf = OP == OP_SOLVE ? P : 0;
+  static constexpr int kVbuf = 0;
   static constexpr int kWarpDoubles = NS * kStageDoubles + kVbuf + 2 * NS;  // + mbarrier slots
   static constexpr int FP = NPAD + 4;  // factor pitch: conflict-free A-fragment reads
   static constexpr int kFacDoubles = OP == OP_PLAIN ? 0 : NPAD * FP + NPAD;
@@ -161,55 +163,61 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
       __syncwarp();
       if (pnl + static_cast<long long>(NS) * NW < npanels) issue(pnl + static_cast<long long>(NS) * NW, s);
     } else if (OP == OP_SOLVE) {
-      constexpr int RL = Cfg::RL;
-      double w[NB][RL];
-      load_panel_regs<NB, RL, PP>(w, stage, g, q);
-      __syncwarp();
-      if (pnl + NW < npanels) issue(pnl + NW, s);
-      // W <- W R^-1, column by column (kernels_scalar.cpp:19-32 order: subtract earlier columns
-      // in ascending order, then scale by the reciprocal diagonal)
-#pragma unroll
-      for (int bc = 0; bc < NB; ++bc) {
-        const int cols_here = min(8, n - 8 * bc);
+      // W <- W R^-1 in place in the stage: lane = row, the whole row in registers, column-order
+      // substitution (kernels_scalar.cpp:19-32: subtract earlier columns ascending, then scale
+      // by the reciprocal diagonal); R is read as shared-memory broadcasts.
+      double* wstage = my + s * Cfg::kStageDoubles;
 #pragma unroll 1
-        for (int gc = 0; gc < cols_here; ++gc) {
-          const int c = 8 * bc + gc;
-          if (g == gc) {
-            const double d = inv[c];
+      for (int r0 = 0; r0 < P; r0 += kWarp) {
+        double* rowp = wstage + r0 + lane;
+        double y[NPAD];
 #pragma unroll
-            for (int t = 0; t < RL / 2; ++t) {
-              w[bc][2 * t] *= d;
-              w[bc][2 * t + 1] *= d;
-              *reinterpret_cast<double2*>(vbuf + 8 * t + 2 * q) =
-                  make_double2(w[bc][2 * t], w[bc][2 * t + 1]);
+        for (int j = 0; j < NPAD; ++j) y[j] = rowp[j * PP];
+        // right-looking form of the same recurrence: once y_i is final, every later column takes
+        // its -r_ij*y_i term (independent FMAs); per column the terms still arrive for ascending i
+        if constexpr (NB <= 6) {
+#pragma unroll
+          for (int i = 0; i < NPAD; ++i) {
+            y[i] *= inv[i];
+            rowp[i * PP] = y[i];
+#pragma unroll
+            for (int j = i + 1; j < NPAD; ++j) y[j] = fma(-fac[i + j * FP], y[i], y[j]);
+          }
+        } else {  // wide rows: left-looking keeps the register pressure (spills) read-only
+#pragma unroll
+          for (int j = 0; j < NPAD; ++j) {
+            double acc0 = y[j], acc1 = 0.0;
+#pragma unroll
+            for (int i = 0; i + 1 < j; i += 2) {
+              acc0 = fma(-fac[i + j * FP], y[i], acc0);
+              acc1 = fma(-fac[i + 1 + j * FP], y[i + 1], acc1);
             }
+            if (j & 1) acc0 = fma(-fac[(j - 1) + j * FP], y[j - 1], acc0);
+            y[j] = (acc0 + acc1) * inv[j];
+            rowp[j * PP] = y[j];
           }
-          __syncwarp();
-          double v[RL];
-#pragma unroll
-          for (int t = 0; t < RL / 2; ++t) {
-            const double2 pv = *reinterpret_cast<const double2*>(vbuf + 8 * t + 2 * q);
-            v[2 * t] = pv.x;
-            v[2 * t + 1] = pv.y;
-          }
-#pragma unroll
-          for (int b = bc; b < NB; ++b) {
-            const int j = 8 * b + g;
-            const double r = (j > c) ? fac[c + j * FP] : 0.0;  // padded columns hold zeros
-#pragma unroll
-            for (int i = 0; i < RL; ++i) w[b][i] = fma(-r, v[i], w[b][i]);
-          }
-          __syncwarp();
         }
       }
+      __syncwarp();
+#pragma unroll 2
+      for (int t = 0; t < P / 8; ++t) {
+        double2 a[NB];
 #pragma unroll
-      for (int i = 0; i < RL; ++i) {
+        for (int b = 0; b < NB; ++b)
+          a[b] = *reinterpret_cast<const double2*>(wstage + (8 * b + g) * PP + 8 * t + 2 * q);
         int p = 0;
 #pragma unroll
         for (int b = 0; b < NB; ++b)
 #pragma unroll
-          for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], w[b][i], w[b2][i]);
+          for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], a[b].x, a[b2].x);
+        p = 0;
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+          for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], a[b].y, a[b2].y);
       }
+      __syncwarp();
+      if (pnl + static_cast<long long>(NS) * NW < npanels) issue(pnl + static_cast<long long>(NS) * NW, s);
     } else {  // OP_MULTIPLY
       const int kchunks = (n + 3) / 4;
       for (int t = 0; t < P / 8; ++t) {
