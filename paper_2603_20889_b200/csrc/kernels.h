@@ -18,6 +18,7 @@ struct TsqrParams {
   int finalize;      // sign-normalise (reference sign_normalize, src/types.cpp:8-14)
   int check_finite;  // raise StatusWord::nonfinite when an Inf/NaN is streamed
   StatusWord* status;
+  int tune = 0;      // experiment switches (SQB_FOLD_TUNE), 0 in production
 };
 cudaError_t launch_tsqr_warp(const TsqrParams& prm, long long num_blocks, cudaStream_t stream);
 int tsqr_warp_panel_rows(int n);
@@ -34,6 +35,18 @@ cudaError_t launch_tsqr_group(const TsqrParams& prm, long long num_blocks, cudaS
 int tsqr_group_chunk_rows(int n);
 int tsqr_group_warps(int n);
 
+// ---- tsqr_fold_kernels.cu (8 < n <= 64: lookahead lane-group kernel with retire loads) --------
+constexpr int kFoldTsqrMinN = 9;
+cudaError_t launch_tsqr_fold(const TsqrParams& prm, long long num_blocks, cudaStream_t stream);
+int tsqr_fold_chunk_rows(int n);
+int tsqr_fold_warps(int n);
+
+// ---- tsqr_mma_kernels.cu (blocked compact-WY Householder on the FP64 tensor cores) ----------
+constexpr int kMmaTsqrMinN = 9;
+cudaError_t launch_tsqr_mma(const TsqrParams& prm, long long num_blocks, cudaStream_t stream);
+int tsqr_mma_panel_rows(int n);
+int tsqr_mma_warps(int n);
+
 // Kernel selection by column count (measured on B200, profiles/): thread-private up to 14 columns,
 // lane groups for 15..24 and 33..64, the warp-panel kernel for 25..32.  SQB_TSQR_KERNEL=0/1/2 forces
 // thread / group / warp-panel where the column count allows it (tuning and A/B tests only).
@@ -43,15 +56,23 @@ inline int tsqr_kernel_kind(int n) {
   if (f == 0 && n <= kThreadTsqrMaxN) return 0;
   if (f == 1 && n > 8) return 1;
   if (f == 2) return 2;
-  if (n <= 14) return 0;
-  if (n <= 24) return 1;
-  if (n <= 32) return 2;
-  return 1;
+  if (f == 3 && n >= kFoldTsqrMinN) return 3;
+  if (f == 4 && n >= kMmaTsqrMinN) return 4;
+  if (f >= 0 && f <= 4) {  // forced kind not available for this n: fall back to the legacy table
+    if (n <= 14) return 0;
+    if (n <= 24) return 1;
+    if (n <= 32) return 2;
+    return 1;
+  }
+  if (n <= 8) return 0;
+  return 3;
 }
 inline cudaError_t launch_tsqr_any(const TsqrParams& prm, long long num_blocks, cudaStream_t stream) {
   switch (tsqr_kernel_kind(prm.n)) {
     case 0: return launch_tsqr_thread(prm, num_blocks, stream);
     case 1: return launch_tsqr_group(prm, num_blocks, stream);
+    case 3: return launch_tsqr_fold(prm, num_blocks, stream);
+    case 4: return launch_tsqr_mma(prm, num_blocks, stream);
     default: return launch_tsqr_warp(prm, num_blocks, stream);
   }
 }
@@ -59,6 +80,8 @@ inline int tsqr_panel_rows(int n) {
   switch (tsqr_kernel_kind(n)) {
     case 0: return tsqr_thread_chunk_rows(n);
     case 1: return tsqr_group_chunk_rows(n);
+    case 3: return tsqr_fold_chunk_rows(n);
+    case 4: return tsqr_mma_panel_rows(n);
     default: return tsqr_warp_panel_rows(n);
   }
 }
@@ -66,6 +89,8 @@ inline int tsqr_warps(int n) {
   switch (tsqr_kernel_kind(n)) {
     case 0: return tsqr_thread_warps(n);
     case 1: return tsqr_group_warps(n);
+    case 3: return tsqr_fold_warps(n);
+    case 4: return tsqr_mma_warps(n);
     default: return tsqr_warp_warps(n);
   }
 }

@@ -1,0 +1,433 @@
+// Lookahead lane-group Q-less Householder TSQR, 8 < n <= 64  ("fold" kernels).
+//
+// Reference semantics: block_qless_qr_core / factor_trapezoidal / make_reflector
+// (reference src/tsqr.cpp:51-158): fold row panels into a running upper triangle with Householder
+// reflectors and discard Q.  TSQR lets the rows be partitioned freely, so a GROUP of G adjacent
+// lanes (G = 1, 2, 4, 16) is one leaf of the reduction tree: it owns P rows per step and a private
+// packed triangle in shared memory; lane g of the group keeps columns g, g+G, g+2G, ... of those
+// rows in registers (w[slot][row]).
+//
+// What is new against tsqr_group_kernels.cu / tsqr_thread_kernels.cu (both FP64-latency bound):
+//   * LOOKAHEAD: step c first applies reflector c to the slot that holds column c+1, then derives
+//     reflector c+1 (norm, sqrt, reciprocal - a ~15-instruction dependent chain) while the
+//     remaining slots are still being updated with reflector c.  Both live in one basic block, so
+//     ptxas interleaves the chain with independent FMAs instead of stalling on it.
+//   * RETIRE LOADS: a slot whose G columns are finished is refilled at once with the rows of the
+//     warp's NEXT chunk (predicated 128-bit streaming loads), so HBM latency hides behind the rest
+//     of the fold without a second register panel or a shared-memory stage.
+//   * a shorter scalar chain (one Goldschmidt step + residual correction, cubic reciprocal step).
+//   * G = 1 (thread-private leaves, no shuffles at all) up to n = 16 with 6-8 rows per step.
+// Per reflector the only communication is the broadcast of the P-entry reflector column from its
+// owner lane (P 64-bit shuffles inside the group, none for G = 1); every dot product is lane-local.
+#include <cstdlib>
+#include <type_traits>
+
+#include "kernels.h"
+
+namespace sqb {
+
+namespace {
+
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
+  }
+}
+
+// Reflector scalars, same contract as make_reflector (common.cuh) with a shorter FP64 chain:
+// MUFU seed (2^-22) -> one coupled Goldschmidt step (2^-43) -> residual correction (norm within
+// 1 ulp); reciprocal of d = a + norm*|pivot| from the MUFU seed with one cubic step (2^-66).
+__device__ __forceinline__ Reflector make_reflector_short(double pivot, double sigma) {
+  Reflector h;
+  const double a = fma(pivot, pivot, sigma);
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  double g = a * y, hh = 0.5 * y;
+  const double r = fma(-g, hh, 0.5);
+  g = fma(g, r, g);
+  hh = fma(hh, r, hh);
+  double norm = fma(fma(-g, g, a), hh, g);
+  const uint32_t ahi = static_cast<uint32_t>(__double2hiint(a));
+  // a > ~1e290: squares about to overflow -> poison (reported as ArgumentError by the epilogue)
+  norm = ahi > 0x7c300000u ? __longlong_as_double(0x7ff8000000000000ll) : norm;
+  const double d = fma(norm, fabs(pivot), a);
+  double z;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(z) : "d"(d));
+  const double e = fma(-d, z, 1.0);
+  const double t = fma(e, e, e);
+  const double inv = fma(z, t, z);
+  const double beta = pivot > 0.0 ? -norm : norm;
+  // identity when the tail is exactly zero or the column is numerically zero (a < ~1e-305)
+  const bool live = (__double_as_longlong(sigma) << 1) != 0 && ahi >= 0x00b00000u;
+  h.beta = live ? beta : pivot;
+  h.u0 = live ? pivot - beta : 0.0;
+  h.gamma = live ? inv : 0.0;
+  return h;
+}
+
+template <int NS, int G, int P, int TMAX>
+struct FoldCfg {
+  static constexpr int NPAD = NS * G;   // columns incl. padding
+  static constexpr int GW = 32 / G;     // groups per warp
+  static constexpr int kTri = NPAD * (NPAD + 1) / 2;
+  // triangle stride == G (mod 16) doubles: the lanes of a half warp hit distinct banks
+  static constexpr int TS = kTri + ((G - kTri % 16) + 16) % 16;
+  static constexpr int kMaxGroups = (227 * 1024) / (TS * 8);
+  // whole multiples of 4 warps: with 6 warps two SM sub-partitions carry two warps and two carry
+  // one, and the FP64 pipe (16 lanes per sub-partition) tops out at 75 % (tools/probe_fp64.cu)
+  static constexpr int kT0 = (kMaxGroups * G) / 128 * 128;
+  static constexpr int T = kT0 < TMAX ? kT0 : TMAX;  // threads per CTA
+  static constexpr int NG = T / G;                    // groups per CTA
+  static constexpr int kChunk = GW * P;               // rows a warp consumes per step
+  static constexpr size_t kSmemBytes = sizeof(double) * TS * NG;
+  static_assert(T >= 64, "too few threads");
+  static_assert(P % 2 == 0, "row pairs");
+};
+
+// two adjacent rows of one column, zero when the predicate is off
+__device__ __forceinline__ void ld2_pred(double& a, double& b, const double* p, int pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %3, 0;\n\t"
+      "mov.f64 %0, 0d0000000000000000;\n\tmov.f64 %1, 0d0000000000000000;\n\t"
+      "@q ld.global.cs.v2.f64 {%0, %1}, [%2];\n\t}"
+      : "=d"(a), "=d"(b)
+      : "l"(p), "r"(pred));
+}
+
+// Where the group's next P rows come from when they can be fetched with aligned 128-bit loads.
+struct NextChunk {
+  const double* base;   // x.base + r_next + 2*grp (row pair of this group in the next chunk)
+  const double* extra;  // same for the optional extra column
+  long long ld;
+  int n_main, n;
+  int pred;             // 0: leave the panel zero (the caller fills it by the generic path)
+};
+
+template <int NS, int G, int P>
+struct Fold {
+  static constexpr int NPAD = NS * G;
+  static constexpr int GW = 32 / G;
+
+  template <int S>
+  static __device__ __forceinline__ void refill(double (&w)[NS][P], const NextChunk& nx, int g) {
+    const int col = S * G + g;
+    const double* cp = col < nx.n_main ? nx.base + static_cast<long long>(col) * nx.ld : nx.extra;
+    const int pred = nx.pred && col < nx.n;
+#pragma unroll
+    for (int k = 0; k < P / 2; ++k) ld2_pred(w[S][2 * k], w[S][2 * k + 1], cp + 2 * GW * k, pred);
+  }
+
+  // column `S`-slot, lane `src` of the group -> v on every lane, plus its reflector
+  template <int S>
+  static __device__ __forceinline__ void head(const double (&w)[NS][P], double (&v)[P], Reflector& h,
+                                              const double* tri, int rowoff, int c, int src) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      v[i] = G > 1 ? __shfl_sync(0xffffffffu, w[S][i], src, G) : w[S][i];
+    }
+#pragma unroll
+    for (int i = 0; i < P; i += 2) {
+      s0 = fma(v[i], v[i], s0);
+      s1 = fma(v[i + 1], v[i + 1], s1);
+    }
+    h = make_reflector_short(tri[rowoff + c], s0 + s1);
+  }
+
+  // One reflector step.  BC = slot of column c; PEEL: c is the last column of its slot (gc == G-1).
+  // Written in phases so that every phase offers (live slots) independent FP64 chains: all dot
+  // products, all update scalars, then the slot of column c+1, the lookahead reflector, the rest.
+  template <int BC, bool PEEL>
+  static __device__ __forceinline__ void step(double (&w)[NS][P], double (&v)[P], Reflector& h,
+                                              double* tri, int& rowoff, int g, int gc,
+                                              const NextChunk& nx) {
+    constexpr int S1 = PEEL ? BC + 1 : BC;   // slot of column c+1
+    constexpr int SLO = PEEL ? BC + 1 : BC;  // first slot that still has live columns
+    constexpr bool HAS_NEXT = S1 < NS;
+    const int c = BC * G + gc;
+    const int gn = PEEL ? 0 : gc + 1;
+    double* rrow = tri + rowoff + g;  // entry (c, s*G+g) at rrow[s*G]
+    const int rowoff_next = rowoff + NPAD - c - 1;
+    double acc[NS];
+    static_for<SLO, NS>([&](auto ss) {
+      constexpr int s = decltype(ss)::value;
+      acc[s] = h.u0 * rrow[s * G];
+    });
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      static_for<SLO, NS>([&](auto ss) {
+        constexpr int s = decltype(ss)::value;
+        acc[s] = fma(v[i], w[s][i], acc[s]);
+      });
+    }
+    static_for<SLO, NS>([&](auto ss) {
+      constexpr int s = decltype(ss)::value;
+      acc[s] *= h.gamma;
+      if (s > BC || g > gc) rrow[s * G] = fma(-h.u0, acc[s], rrow[s * G]);
+    });
+    Reflector hn;
+    if constexpr (HAS_NEXT) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) w[S1][i] = fma(-v[i], acc[S1], w[S1][i]);
+      // lookahead: reflector c+1 from the freshly updated column, overlapped with the updates below
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < P; i += 2) {
+        s0 = fma(w[S1][i], w[S1][i], s0);
+        s1 = fma(w[S1][i + 1], w[S1][i + 1], s1);
+      }
+      double sig = s0 + s1;
+      if constexpr (G > 1) sig = __shfl_sync(0xffffffffu, sig, gn, G);
+#ifdef SQB_FOLD_NOCHAIN
+      hn.beta = sig; hn.u0 = tri[rowoff_next + c + 1]; hn.gamma = 1e-300 * sig;
+#else
+      hn = make_reflector_short(tri[rowoff_next + c + 1], sig);
+#endif
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      static_for<SLO, NS>([&](auto ss) {
+        constexpr int s = decltype(ss)::value;
+        if constexpr (!(HAS_NEXT && s == S1)) w[s][i] = fma(-v[i], acc[s], w[s][i]);
+      });
+    }
+    if (g == gc) tri[rowoff + c] = h.beta;
+    if constexpr (PEEL && BC < NS - 1) refill<BC>(w, nx, g);
+    if constexpr (HAS_NEXT) {
+      if constexpr (G > 1) {
+#pragma unroll
+        for (int i = 0; i < P; ++i) v[i] = __shfl_sync(0xffffffffu, w[S1][i], gn, G);
+      } else {
+#pragma unroll
+        for (int i = 0; i < P; ++i) v[i] = w[S1][i];
+      }
+      h = hn;
+    }
+    rowoff = rowoff_next;
+  }
+
+  // Fold the group's P x n register panel into its triangle; on return the panel holds the rows
+  // named by `nx` (or zeros).
+  static __device__ __forceinline__ void run(double (&w)[NS][P], double* tri, int n, int g,
+                                             const NextChunk& nx) {
+    double v[P];
+    Reflector h;
+    int rowoff = 0;
+    if constexpr (G > 1) __syncwarp();  // pivots written by other lanes in the previous fold
+    head<0>(w, v, h, tri, 0, 0, 0);
+    static_for<0, NS>([&](auto bb) {
+      constexpr int bc = decltype(bb)::value;
+      if constexpr (bc < NS - 1) {
+        if constexpr (G > 1) {
+#pragma unroll 1
+          for (int gc = 0; gc < G - 1; ++gc) step<bc, false>(w, v, h, tri, rowoff, g, gc, nx);
+        }
+        step<bc, true>(w, v, h, tri, rowoff, g, G - 1, nx);
+      } else {
+        const int cols_last = n - bc * G;  // 1..G live columns in the last slot
+        if constexpr (G > 1) {
+          const int lim = cols_last < G - 1 ? cols_last : G - 1;
+#pragma unroll 1
+          for (int gc = 0; gc < lim; ++gc) step<bc, false>(w, v, h, tri, rowoff, g, gc, nx);
+        }
+        if (cols_last == G) step<bc, true>(w, v, h, tri, rowoff, g, G - 1, nx);
+        refill<bc>(w, nx, g);
+      }
+    });
+  }
+};
+
+template <int NS, int G, int P, int TMAX>
+__global__ void __launch_bounds__(FoldCfg<NS, G, P, TMAX>::T, 1) tsqr_fold_kernel(const TsqrParams prm) {
+  using Cfg = FoldCfg<NS, G, P, TMAX>;
+  constexpr int T = Cfg::T, NW = T / 32, GW = Cfg::GW, CH = Cfg::kChunk, NPAD = Cfg::NPAD;
+  constexpr int TS = Cfg::TS, NG = Cfg::NG;
+  extern __shared__ __align__(16) double tris[];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane % G, grp = lane / G;  // lane inside group, group inside warp
+  const int gid = tid / G;                 // group inside CTA
+  const int n = prm.n;
+  double* tri = tris + static_cast<size_t>(gid) * TS;
+  for (int e = g; e < TS; e += G) tri[e] = 0.0;
+
+  const long long blk = blockIdx.x;
+  const long long begin = min(blk * prm.rows_per_block, prm.m);
+  const long long end = min((blk + 1) * prm.rows_per_block, prm.m);
+  const long long nchunks = (end - begin + CH - 1) / CH;
+  const bool aligned = view_bulk_aligned(prm.x, n, begin);
+
+  NextChunk nx;
+  nx.ld = prm.x.ld;
+  nx.n_main = prm.x.n_main;
+  nx.n = n;
+
+  double w[NS][P];
+  bool loaded = false;  // the panel already holds the rows of chunk `ch`
+
+  // ---- stream the block's rows ------------------------------------------------------------------
+  for (long long ch = warp; ch < nchunks; ch += NW) {
+    const long long r0 = begin + ch * CH;
+    if (!loaded) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const int col = s * G + g;
+        const double* cp = prm.x.col(col < n ? col : 0);
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          const long long row = r0 + 2 * GW * (i >> 1) + 2 * grp + (i & 1);
+          w[s][i] = (col < n && row < end) ? __ldg(cp + row) : 0.0;
+        }
+      }
+    }
+    const long long rn = r0 + static_cast<long long>(NW) * CH;  // the warp's next chunk
+    const bool fast = aligned && rn + CH <= end;
+    if (fast && !(prm.tune & 1) && rn + static_cast<long long>(NW + 1) * CH <= end) {
+      // pull the chunk after the next one towards L2
+      for (int j = lane; j < n; j += 32) {
+        const double* nxt = prm.x.col(j) + rn + static_cast<long long>(NW) * CH;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt), "r"(CH * 8) : "memory");
+      }
+    }
+    nx.base = prm.x.base + rn + 2 * grp;
+    nx.extra = prm.x.extra + rn + 2 * grp;
+    nx.pred = fast ? 1 : 0;
+    Fold<NS, G, P>::run(w, tri, n, g, nx);
+    loaded = fast;
+  }
+
+  // ---- merge the CTA's group triangles: shared-memory tree, same folding routine ------------------
+  nx.pred = 0;
+  int active = NG;
+  while (active > 1) {
+    const int half = (active + 1) / 2;
+    __syncthreads();
+    // a warp takes part when any of its groups has a partner; groups without one fold zero rows
+    const bool has = gid < active - half;
+    const bool warp_has = (warp * GW) < active - half;
+    if (warp_has) {
+      const double* other = tris + static_cast<size_t>(has ? gid + half : gid) * TS;
+#pragma unroll 1
+      for (int base = 0; base < n; base += P) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+#pragma unroll
+          for (int i = 0; i < P; ++i) {
+            const int row = base + i, col = s * G + g;
+            w[s][i] = (has && row <= col && row < n) ? other[row_base(row, NPAD) + col] : 0.0;
+          }
+        Fold<NS, G, P>::run(w, tri, n, g, nx);
+      }
+    }
+    active = half;
+  }
+  __syncthreads();
+
+  // ---- CTA triangle -> rows [blk*n, blk*n+n) of Y (full square, zeros below the diagonal) ---------
+  double* dst = prm.y + blk * n;
+  bool bad = false;
+  for (int idx = tid; idx < n * n; idx += T) {
+    const int i = idx % n, j = idx / n;
+    double val = 0.0;
+    if (i <= j) {
+      val = tris[row_base(i, NPAD) + j];
+      bad = bad || is_nonfinite(val);
+      if (prm.finalize && tris[row_base(i, NPAD) + i] < 0.0) val = -val;
+    }
+    dst[i + j * prm.ldy] = val;
+  }
+  if (prm.check_finite && bad) atomicExch(&prm.status->nonfinite, 1);
+}
+
+template <int NS, int G, int P, int TMAX>
+cudaError_t launch_cfg(const TsqrParams& prm, long long num_blocks, cudaStream_t stream) {
+  using Cfg = FoldCfg<NS, G, P, TMAX>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(tsqr_fold_kernel<NS, G, P, TMAX>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(Cfg::kSmemBytes));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  tsqr_fold_kernel<NS, G, P, TMAX>
+      <<<static_cast<unsigned>(num_blocks), Cfg::T, Cfg::kSmemBytes, stream>>>(prm);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// column count -> (slots per lane, lanes per group, rows per step, max threads per CTA)
+#define SQB_FOLD_SWITCH(EXPR)                 \
+  switch (n) {                                \
+    case 9: return EXPR(9, 1, 8, 256);        \
+    case 10: return EXPR(10, 1, 8, 256);      \
+    case 11: return EXPR(11, 1, 8, 256);      \
+    case 12: return EXPR(12, 1, 8, 256);      \
+    case 13: return EXPR(13, 1, 6, 256);      \
+    case 14: return EXPR(14, 1, 6, 256);      \
+    case 15: return EXPR(15, 1, 6, 256);      \
+    case 16: return EXPR(16, 1, 6, 256);      \
+    default: break;                           \
+  }                                           \
+  if (n <= 18) return EXPR(9, 2, 8, 256);     \
+  if (n <= 20) return EXPR(10, 2, 8, 256);    \
+  if (n <= 22) return EXPR(11, 2, 8, 256);    \
+  if (n <= 24) return EXPR(12, 2, 8, 256);    \
+  if (n <= 28) return EXPR(7, 4, 12, 256);    \
+  if (n <= 32) return EXPR(8, 4, 12, 256);    \
+  if (n <= 48) return EXPR(3, 16, 16, 256);   \
+  return EXPR(4, 16, 16, 256);
+
+#ifdef SQB_FOLD_EXPERIMENT
+static int fold_variant() {
+  static int v = [] { const char* e = getenv("SQB_FOLD_VARIANT"); return e ? atoi(e) : 0; }();
+  return v;
+}
+#define SQB_FOLD_EXPERIMENTS(EXPR)                                                        \
+  {                                                                                       \
+    const int v = fold_variant();                                                         \
+    if (n == 12) switch (v) { case 1: return EXPR(12, 1, 6, 256); case 2: return EXPR(12, 1, 4, 256); \
+        case 3: return EXPR(6, 2, 16, 256); case 4: return EXPR(6, 2, 12, 256); default: break; }     \
+    if (n == 16) switch (v) { case 1: return EXPR(16, 1, 4, 128); case 2: return EXPR(8, 2, 8, 256);  \
+        case 3: return EXPR(8, 2, 12, 256); case 4: return EXPR(4, 4, 16, 256); case 5: return EXPR(16, 1, 6, 128); default: break; } \
+    if (n == 32) switch (v) { case 1: return EXPR(8, 4, 12, 128); case 2: return EXPR(8, 4, 8, 128);  \
+        case 3: return EXPR(4, 8, 16, 256); case 4: return EXPR(4, 8, 24, 256); default: break; }     \
+  }
+#else
+#define SQB_FOLD_EXPERIMENTS(EXPR)
+#endif
+
+static int fold_tune() {
+  static int v = [] { const char* e = getenv("SQB_FOLD_TUNE"); return e ? atoi(e) : 0; }();
+  return v;
+}
+
+cudaError_t launch_tsqr_fold(const TsqrParams& prm_in, long long num_blocks, cudaStream_t stream) {
+  TsqrParams prm = prm_in;
+  prm.tune = fold_tune();
+  const int n = prm.n;
+  if (n < kFoldTsqrMinN || n > 64) return cudaErrorInvalidValue;
+#define LG(NSV, GV, PV, TV) launch_cfg<NSV, GV, PV, TV>(prm, num_blocks, stream)
+  SQB_FOLD_EXPERIMENTS(LG)
+  SQB_FOLD_SWITCH(LG)
+#undef LG
+}
+
+int tsqr_fold_chunk_rows(int n) {
+#define CG(NSV, GV, PV, TV) FoldCfg<NSV, GV, PV, TV>::kChunk
+  SQB_FOLD_EXPERIMENTS(CG)
+  SQB_FOLD_SWITCH(CG)
+#undef CG
+}
+
+int tsqr_fold_warps(int n) {
+#define WG(NSV, GV, PV, TV) (FoldCfg<NSV, GV, PV, TV>::T / 32)
+  SQB_FOLD_EXPERIMENTS(WG)
+  SQB_FOLD_SWITCH(WG)
+#undef WG
+}
+
+}  // namespace sqb

@@ -328,9 +328,9 @@ def test_device_lstsq_with_constant_rhs(ctx, oracle, n):
         assert abs(float(res.item()) - res_ref) <= 1e-10 * res_ref
 
 
-@pytest.mark.parametrize("kind", ["0", "1", "2"])
+@pytest.mark.parametrize("kind", ["0", "1", "2", "3", "4"])
 def test_every_tsqr_kernel_family(kind, oracle):
-    """The three TSQR kernel families (thread / lane-group / warp-panel) on the same inputs, forced
+    """The TSQR kernel families (thread / lane-group / warp-panel / lookahead fold / DMMA blocked) on the same inputs, forced
     through SQB_TSQR_KERNEL in a fresh process so that the measured selection table is bypassed."""
     import subprocess
     import sys
@@ -340,7 +340,7 @@ def test_every_tsqr_kernel_family(kind, oracle):
         "import oracle, paper_2603_20889_b200 as sq\n"
         "from conftest import gaussian, r_bound\n"
         "ctx = sq.default_context()\n"
-        "for m, n in [(9000, 5), (9001, 11), (20000, 16), (7000, 24), (6000, 33), (5000, 64)]:\n"
+        "for m, n in [(9000, 5), (9001, 11), (20000, 16), (30011, 17), (7000, 24), (40000, 29), (40002, 32), (6000, 33), (9000, 47), (5000, 64), (70000, 64)]:\n"
         "    x = gaussian(m, n, seed=n); x[:, n // 2] = 1.0\n"
         "    r = ctx.tsqr_qless(x)\n"
         "    assert np.linalg.norm(r - oracle.port.reference_hhqr(x)) <= r_bound(x), (m, n)\n"
