@@ -38,24 +38,31 @@ def _stale(target: Path, deps) -> bool:
     return any(Path(d).stat().st_mtime > t for d in deps)
 
 
+# (8-column tiles, 8-row groups per panel, warps per CTA) instances of the DMMA TSQR kernel, one
+# translation unit each (tsqr_mma_inst.cu) - keep in sync with SQB_MMA_CONFIGS in tsqr_mma_kernels.cu
+MMA_CONFIGS = [(2, 8, 8), (3, 8, 8), (4, 8, 8), (5, 6, 8), (6, 6, 8), (7, 6, 8), (8, 6, 8)]
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     OBJ.mkdir(exist_ok=True)
     headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + list(INCLUDE.glob("*.h"))
     nvcc = _nvcc()
     jobs = []
-    for src in SOURCES:
-        obj = OBJ / (src[:-3] + ".o")
+    units = [(src, [], OBJ / (src[:-3] + ".o")) for src in SOURCES]
+    units += [("tsqr_mma_inst.cu", [f"-DSQB_MMA_NB={nb}", f"-DSQB_MMA_RG={rg}", f"-DSQB_MMA_NW={nw}"],
+               OBJ / f"tsqr_mma_{nb}_{rg}_{nw}.o") for nb, rg, nw in MMA_CONFIGS]
+    for src, defs, obj in units:
         if force or _stale(obj, [CSRC / src] + headers):
-            cmd = [nvcc] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-c", str(CSRC / src), "-o", str(obj)]
+            cmd = [nvcc] + NVCC_FLAGS + defs + (["-Xptxas", "-v"] if verbose else []) + ["-c", str(CSRC / src), "-o", str(obj)]
             jobs.append(cmd)
     if jobs:
-        with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
+        with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
             for res in ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), jobs):
                 if verbose or res.returncode != 0:
                     sys.stderr.write(res.stdout + res.stderr)
                 if res.returncode != 0:
                     raise RuntimeError("nvcc failed: " + " ".join(res.args))
-    objs = [str(OBJ / (s[:-3] + ".o")) for s in SOURCES]
+    objs = [str(obj) for _, _, obj in units]
     if force or jobs or _stale(OUT, objs):
         cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(OUT)] + objs + ["-ldl"]
         res = subprocess.run(cmd, capture_output=True, text=True)

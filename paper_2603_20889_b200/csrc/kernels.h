@@ -47,9 +47,10 @@ cudaError_t launch_tsqr_mma(const TsqrParams& prm, long long num_blocks, cudaStr
 int tsqr_mma_panel_rows(int n);
 int tsqr_mma_warps(int n);
 
-// Kernel selection by column count (measured on B200, profiles/): thread-private up to 14 columns,
-// lane groups for 15..24 and 33..64, the warp-panel kernel for 25..32.  SQB_TSQR_KERNEL=0/1/2 forces
-// thread / group / warp-panel where the column count allows it (tuning and A/B tests only).
+// Kernel selection by column count (measured on B200, profiles/README.md): register-resident thread
+// kernel up to 8 columns, lookahead fold kernel for 9..28, DMMA blocked kernel for 29..64.
+// SQB_TSQR_KERNEL=0..4 forces thread / lane-group / warp-panel / fold / DMMA where the column count
+// allows it (tuning, A/B tests and the kernel-family parity test only).
 int tsqr_forced_kind();
 inline int tsqr_kernel_kind(int n) {
   const int f = tsqr_forced_kind();
@@ -65,7 +66,8 @@ inline int tsqr_kernel_kind(int n) {
     return 1;
   }
   if (n <= 8) return 0;
-  return 3;
+  if (n <= 28) return 3;
+  return 4;
 }
 inline cudaError_t launch_tsqr_any(const TsqrParams& prm, long long num_blocks, cudaStream_t stream) {
   switch (tsqr_kernel_kind(prm.n)) {

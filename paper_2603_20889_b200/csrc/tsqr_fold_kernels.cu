@@ -359,7 +359,10 @@ cudaError_t launch_cfg(const TsqrParams& prm, long long num_blocks, cudaStream_t
 
 }  // namespace
 
-// column count -> (slots per lane, lanes per group, rows per step, max threads per CTA)
+// column count -> (slots per lane, lanes per group, rows per step, max threads per CTA); measured
+// on B200 (gpurun_out/fold_select.txt, profiles/README.md): thread-private leaves up to 14 columns,
+// lane pairs up to 20, lane quads up to 28; above that the DMMA kernel (tsqr_mma_kernels.cu) wins
+// and the last three rows only serve SQB_TSQR_KERNEL=3
 #define SQB_FOLD_SWITCH(EXPR)                 \
   switch (n) {                                \
     case 9: return EXPR(9, 1, 8, 256);        \
@@ -368,14 +371,12 @@ cudaError_t launch_cfg(const TsqrParams& prm, long long num_blocks, cudaStream_t
     case 12: return EXPR(12, 1, 8, 256);      \
     case 13: return EXPR(13, 1, 6, 256);      \
     case 14: return EXPR(14, 1, 6, 256);      \
-    case 15: return EXPR(15, 1, 6, 256);      \
-    case 16: return EXPR(16, 1, 6, 256);      \
     default: break;                           \
   }                                           \
+  if (n <= 16) return EXPR(8, 2, 12, 256);    \
   if (n <= 18) return EXPR(9, 2, 8, 256);     \
   if (n <= 20) return EXPR(10, 2, 8, 256);    \
-  if (n <= 22) return EXPR(11, 2, 8, 256);    \
-  if (n <= 24) return EXPR(12, 2, 8, 256);    \
+  if (n <= 24) return EXPR(6, 4, 12, 256);    \
   if (n <= 28) return EXPR(7, 4, 12, 256);    \
   if (n <= 32) return EXPR(8, 4, 12, 256);    \
   if (n <= 48) return EXPR(3, 16, 16, 256);   \
@@ -389,12 +390,24 @@ static int fold_variant() {
 #define SQB_FOLD_EXPERIMENTS(EXPR)                                                        \
   {                                                                                       \
     const int v = fold_variant();                                                         \
-    if (n == 12) switch (v) { case 1: return EXPR(12, 1, 6, 256); case 2: return EXPR(12, 1, 4, 256); \
-        case 3: return EXPR(6, 2, 16, 256); case 4: return EXPR(6, 2, 12, 256); default: break; }     \
-    if (n == 16) switch (v) { case 1: return EXPR(16, 1, 4, 128); case 2: return EXPR(8, 2, 8, 256);  \
-        case 3: return EXPR(8, 2, 12, 256); case 4: return EXPR(4, 4, 16, 256); case 5: return EXPR(16, 1, 6, 128); default: break; } \
-    if (n == 32) switch (v) { case 1: return EXPR(8, 4, 12, 128); case 2: return EXPR(8, 4, 8, 128);  \
-        case 3: return EXPR(4, 8, 16, 256); case 4: return EXPR(4, 8, 24, 256); default: break; }     \
+    const int h = (n + 1) / 2;                                                            \
+    if (v == 1 && n <= 24) switch (h) {                                                   \
+        case 5: return EXPR(5, 2, 8, 256); case 6: return EXPR(6, 2, 8, 256); case 7: return EXPR(7, 2, 8, 256); \
+        case 8: return EXPR(8, 2, 8, 256); case 9: return EXPR(9, 2, 8, 256); case 10: return EXPR(10, 2, 8, 256); \
+        case 11: return EXPR(11, 2, 8, 256); case 12: return EXPR(12, 2, 8, 256); default: break; }     \
+    if (v == 2 && n <= 20) switch (h) {                                                   \
+        case 5: return EXPR(5, 2, 12, 256); case 6: return EXPR(6, 2, 12, 256); case 7: return EXPR(7, 2, 12, 256); \
+        case 8: return EXPR(8, 2, 12, 256); case 9: return EXPR(9, 2, 12, 256); case 10: return EXPR(10, 2, 12, 256); \
+        default: break; }                                                                 \
+    if (v == 3 && n <= 16) switch (h) {                                                   \
+        case 5: return EXPR(5, 2, 16, 256); case 6: return EXPR(6, 2, 16, 256); case 7: return EXPR(7, 2, 16, 256); \
+        case 8: return EXPR(8, 2, 16, 256); default: break; }                             \
+    if (v == 4 && n > 16 && n <= 32) { const int f = (n + 3) / 4; switch (f) {            \
+        case 5: return EXPR(5, 4, 12, 256); case 6: return EXPR(6, 4, 12, 256); case 7: return EXPR(7, 4, 12, 256); \
+        case 8: return EXPR(8, 4, 12, 256); default: break; } }                           \
+    if (v == 5 && n > 16 && n <= 32) { const int f = (n + 3) / 4; switch (f) {            \
+        case 5: return EXPR(5, 4, 16, 256); case 6: return EXPR(6, 4, 16, 256); case 7: return EXPR(7, 4, 8, 256); \
+        case 8: return EXPR(8, 4, 8, 256); default: break; } }                            \
   }
 #else
 #define SQB_FOLD_EXPERIMENTS(EXPR)

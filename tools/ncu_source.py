@@ -36,3 +36,12 @@ if "--dump" in sys.argv:
     lo, hi = int(sys.argv[sys.argv.index("--dump")+1]), int(sys.argv[sys.argv.index("--dump")+2])
     for d in data[lo:hi]:
         print(f"  #{d[0]:5d} ex={d[2]:8d} s={d[3]:5d} {d[1][:90]}")
+if "--byop" in sys.argv:
+    byop = collections.Counter(); cnt = collections.Counter()
+    for d in data:
+        op = d[1].split()
+        name = op[1] if op and op[0].startswith("@") else (op[0] if op else "?")
+        byop[name.split(".")[0]] += d[3]; cnt[name.split(".")[0]] += d[2]
+    print("samples by opcode (where warps sit):")
+    for name, c in byop.most_common(16):
+        print(f"  {name:10s} samples {c:8d} {100.0*c/tot_s:5.1f}%   executed {cnt[name]:12d}  samples/1k-exec {1000.0*c/max(cnt[name],1):7.2f}")
