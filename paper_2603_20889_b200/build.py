@@ -16,7 +16,7 @@ CSRC = PKG / "csrc"
 OUT = PKG / "libskinnyqr_b200.so"
 OBJ = PKG / "build"
 INCLUDE = PKG.parent / "include"
-SOURCES = ["tsqr_kernels.cu", "tsqr_thread_kernels.cu", "tsqr_group_kernels.cu", "tsqr_fold_kernels.cu", "tsqr_mma_kernels.cu", "gram_kernels.cu", "gram_thread_kernels.cu", "small_kernels.cu", "matgen_kernels.cu", "capi.cu"]
+SOURCES = ["tsqr_kernels.cu", "tsqr_thread_kernels.cu", "tsqr_group_kernels.cu", "tsqr_fold_kernels.cu", "tsqr_mma_kernels.cu", "gram_kernels.cu", "gram_wide_kernels.cu", "gram_thread_kernels.cu", "small_kernels.cu", "matgen_kernels.cu", "capi.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
     "-Xcompiler", "-fPIC", "-I", str(INCLUDE), "-I", str(CSRC),

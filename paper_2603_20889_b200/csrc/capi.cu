@@ -496,7 +496,17 @@ static int gram_entry(sqb_context* ctx, const double* d_x, int64_t m, int64_t n,
                       const double* factor, int64_t k, int64_t b, double* d_c) {
   SQB_TRY(enter(ctx));
   if (n < 1 || m < 0) return SQB_E_DIMENSION;
-  if (n > 64 || ld < m) return SQB_E_ARGUMENT;
+  if (ld < m) return SQB_E_ARGUMENT;
+  if (n > 64) {
+    // the reference's tsmttsm has no column limit (gram.cpp:113-121); the fused variants stay at
+    // n <= 64 here (register / shared-memory tiles), the plain Gram goes up to 256 columns
+    if (op != OP_PLAIN || n > kWideGramMaxN) return SQB_E_ARGUMENT;
+    const int nn = static_cast<int>(n);
+    SQB_TRY(grow(&ctx->work, &ctx->work_doubles, gram_wide_partial_doubles(nn, ctx->sm_count)));
+    SQB_CUDA(launch_gram_wide(d_x, m, nn, ld, ctx->sm_count, ctx->work, d_c, 1, ctx->d_status, ctx->stream));
+    ctx->launches += 2;
+    return SQB_OK;
+  }
   if (op == OP_MULTIPLY) {  // tsmmttsmm checks B for finiteness (gram.cpp:143-145)
     SQB_CUDA(launch_check_finite(factor, n * n, ctx->d_status, ctx->stream));
     ctx->launches++;
@@ -691,7 +701,7 @@ static int gram_host(sqb_context* ctx, const double* x, int64_t m, int64_t n, in
                      const double* factor, int64_t k, int64_t b, double* c) {
   SQB_TRY(enter(ctx));
   if (n < 1 || m < 0) return SQB_E_DIMENSION;
-  if (n > 64 || ld < m) return SQB_E_ARGUMENT;
+  if (n > (op == OP_PLAIN ? kWideGramMaxN : 64) || ld < m) return SQB_E_ARGUMENT;
   const int nn = static_cast<int>(n);
   Small s;
   SQB_TRY(small_slots(ctx, nn, &s));

@@ -101,42 +101,44 @@ constexpr uint32_t kNonFiniteHi = 0x7ff00000u;
 // gives the identity (gamma = u0 = 0, beta = pivot) so a zero column keeps an exact zero diagonal.
 //
 // The scalar chain is the serial bottleneck of every Householder kernel here, so it is short and
-// BRANCH-FREE (one basic block per fold lets ptxas overlap it with the trailing updates):
-// Goldschmidt sqrt/rsqrt from the MUFU seed (two coupled iterations + one residual correction:
-// norm within 1 ulp) and a Newton reciprocal.  Inf/NaN propagate through it into R, which is how
-// non-finite input is detected.  Guards: a = pivot^2 + sigma below 1e-305 (the reciprocal would
-// overflow; such a column is numerically zero) gives the identity; above 1e290 (squares about to
-// overflow - the reference's plain dot products are garbage there as well) norm is poisoned with
-// NaN so that the call reports ArgumentError instead of a silently wrong R.
+// BRANCH-FREE (one basic block per fold lets ptxas overlap it with the trailing updates): MUFU
+// rsqrt seed (2^-22) -> one coupled Goldschmidt step (2^-43) -> residual correction (norm within
+// 1 ulp); the reciprocal seed is taken from the first norm estimate, so that both MUFU results
+// arrive while the Goldschmidt step runs, and finished with one cubic step on the exact
+// d = a + norm*|pivot| (2^-63).  Inf/NaN propagate through it into R, which is how non-finite input
+// is detected.  Guards: a = pivot^2 + sigma below ~1e-305 (the reciprocal would overflow; such a
+// column is numerically zero) gives the identity; above ~1e290 (squares about to overflow - the
+// reference's plain dot products are garbage there as well) beta is poisoned with NaN so that the
+// call reports ArgumentError instead of a silently wrong R.  The exponent tests run on the integer
+// pipe and, like the identity selects, sit off the path that leads to gamma.
 struct Reflector {
   double beta, u0, gamma;
 };
 __device__ __forceinline__ Reflector make_reflector(double pivot, double sigma) {
   Reflector h;
+  const double ap = fabs(pivot);
   const double a = fma(pivot, pivot, sigma);
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
   double g = a * y, hh = 0.5 * y;
-  double r = fma(-g, hh, 0.5);
-  g = fma(g, r, g);
-  hh = fma(hh, r, hh);
-  r = fma(-g, hh, 0.5);
-  g = fma(g, r, g);
-  hh = fma(hh, r, hh);
-  double norm = fma(fma(-g, g, a), hh, g);
-  norm = a > 1e290 ? __longlong_as_double(0x7ff8000000000000ll) : norm;
-  const double d = norm * (norm + fabs(pivot));
+  const double da = fma(g, ap, a);
   double z;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(z) : "d"(d));
-  double e = fma(-d, z, 1.0);
-  z = fma(z, e, z);
-  e = fma(-d, z, 1.0);
-  const double inv = fma(z, e, z);
-  const double beta = pivot > 0.0 ? -norm : norm;
-  const bool live = sigma != 0.0 && !(a < 1e-305);
-  h.beta = live ? beta : pivot;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(z) : "d"(da));
+  const double r = fma(-g, hh, 0.5);
+  g = fma(g, r, g);
+  hh = fma(hh, r, hh);
+  const double norm = fma(fma(-g, g, a), hh, g);
+  const double d = fma(norm, ap, a);
+  const double e = fma(-d, z, 1.0);
+  const double t = fma(e, e, e);
+  const double inv = fma(z, t, z);
+  const uint32_t ahi = static_cast<uint32_t>(__double2hiint(a));
+  const bool live = (__double_as_longlong(sigma) << 1) != 0 && ahi >= 0x00b00000u;
+  double beta = pivot > 0.0 ? -norm : norm;
   h.u0 = live ? pivot - beta : 0.0;
   h.gamma = live ? inv : 0.0;
+  beta = ahi > 0x7c300000u ? __longlong_as_double(0x7ff8000000000000ll) : beta;
+  h.beta = live ? beta : pivot;
   return h;
 }
 

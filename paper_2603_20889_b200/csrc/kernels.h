@@ -116,6 +116,12 @@ int gram_panel_rows(int n, int op);
 int gram_warps(int n);
 int gram_ctas_per_sm(int n, int op);
 
+// ---- gram_wide_kernels.cu (64 < n <= 256, plain Gram only: BASELINE config 5) -----------------
+constexpr int kWideGramMaxN = 256;
+size_t gram_wide_partial_doubles(int n, int sm_count);
+cudaError_t launch_gram_wide(const double* x, long long m, int n, long long ld, int sm_count, double* partial,
+                             double* c, int check_finite, StatusWord* status, cudaStream_t stream);
+
 // ---- gram_thread_kernels.cu (n <= 8: register-resident rows and accumulators) --------------
 constexpr int kThreadGramMaxN = 8;
 cudaError_t launch_gram_thread(const GramParams& prm, int op, long long num_blocks,

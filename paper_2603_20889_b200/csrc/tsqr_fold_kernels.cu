@@ -15,7 +15,6 @@
 //   * RETIRE LOADS: a slot whose G columns are finished is refilled at once with the rows of the
 //     warp's NEXT chunk (predicated 128-bit streaming loads), so HBM latency hides behind the rest
 //     of the fold without a second register panel or a shared-memory stage.
-//   * a shorter scalar chain (one Goldschmidt step + residual correction, cubic reciprocal step).
 //   * G = 1 (thread-private leaves, no shuffles at all) up to n = 16 with 6-8 rows per step.
 // Per reflector the only communication is the broadcast of the P-entry reflector column from its
 // owner lane (P 64-bit shuffles inside the group, none for G = 1); every dot product is lane-local.
@@ -34,37 +33,6 @@ __device__ __forceinline__ void static_for(F&& f) {
     f(std::integral_constant<int, B>{});
     static_for<B + 1, E>(f);
   }
-}
-
-// Reflector scalars, same contract as make_reflector (common.cuh) with a shorter FP64 chain:
-// MUFU seed (2^-22) -> one coupled Goldschmidt step (2^-43) -> residual correction (norm within
-// 1 ulp); reciprocal of d = a + norm*|pivot| from the MUFU seed with one cubic step (2^-66).
-__device__ __forceinline__ Reflector make_reflector_short(double pivot, double sigma) {
-  Reflector h;
-  const double a = fma(pivot, pivot, sigma);
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
-  double g = a * y, hh = 0.5 * y;
-  const double r = fma(-g, hh, 0.5);
-  g = fma(g, r, g);
-  hh = fma(hh, r, hh);
-  double norm = fma(fma(-g, g, a), hh, g);
-  const uint32_t ahi = static_cast<uint32_t>(__double2hiint(a));
-  // a > ~1e290: squares about to overflow -> poison (reported as ArgumentError by the epilogue)
-  norm = ahi > 0x7c300000u ? __longlong_as_double(0x7ff8000000000000ll) : norm;
-  const double d = fma(norm, fabs(pivot), a);
-  double z;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(z) : "d"(d));
-  const double e = fma(-d, z, 1.0);
-  const double t = fma(e, e, e);
-  const double inv = fma(z, t, z);
-  const double beta = pivot > 0.0 ? -norm : norm;
-  // identity when the tail is exactly zero or the column is numerically zero (a < ~1e-305)
-  const bool live = (__double_as_longlong(sigma) << 1) != 0 && ahi >= 0x00b00000u;
-  h.beta = live ? beta : pivot;
-  h.u0 = live ? pivot - beta : 0.0;
-  h.gamma = live ? inv : 0.0;
-  return h;
 }
 
 template <int NS, int G, int P, int TMAX>
@@ -133,7 +101,7 @@ struct Fold {
       s0 = fma(v[i], v[i], s0);
       s1 = fma(v[i + 1], v[i + 1], s1);
     }
-    h = make_reflector_short(tri[rowoff + c], s0 + s1);
+    h = make_reflector(tri[rowoff + c], s0 + s1);
   }
 
   // One reflector step.  BC = slot of column c; PEEL: c is the last column of its slot (gc == G-1).
@@ -183,7 +151,7 @@ struct Fold {
 #ifdef SQB_FOLD_NOCHAIN
       hn.beta = sig; hn.u0 = tri[rowoff_next + c + 1]; hn.gamma = 1e-300 * sig;
 #else
-      hn = make_reflector_short(tri[rowoff_next + c + 1], sig);
+      hn = make_reflector(tri[rowoff_next + c + 1], sig);
 #endif
     }
 #pragma unroll

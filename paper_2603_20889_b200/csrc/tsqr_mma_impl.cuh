@@ -45,39 +45,6 @@ __device__ __forceinline__ void static_for(F&& f) {
   }
 }
 
-// Same contract as make_reflector (common.cuh), arranged for the shortest dependent chain: the
-// reciprocal seed is taken from the first norm estimate (so both MUFU results arrive while the
-// Goldschmidt step runs) and finished with one cubic step on the exact d = a + norm*|pivot|;
-// the overflow poison and the identity selects sit off the path that leads to gamma.
-__device__ __forceinline__ Reflector make_reflector_mma(double pivot, double sigma) {
-  Reflector h;
-  const double ap = fabs(pivot);
-  const double a = fma(pivot, pivot, sigma);
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
-  double g = a * y, hh = 0.5 * y;
-  const double da = fma(g, ap, a);
-  double z;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(z) : "d"(da));
-  const double r = fma(-g, hh, 0.5);
-  g = fma(g, r, g);
-  hh = fma(hh, r, hh);
-  const double norm = fma(fma(-g, g, a), hh, g);
-  const double d = fma(norm, ap, a);
-  const double e = fma(-d, z, 1.0);
-  const double t = fma(e, e, e);
-  const double inv = fma(z, t, z);
-  const uint32_t ahi = static_cast<uint32_t>(__double2hiint(a));
-  const bool live = (__double_as_longlong(sigma) << 1) != 0 && ahi >= 0x00b00000u;
-  double beta = pivot > 0.0 ? -norm : norm;
-  h.u0 = live ? pivot - beta : 0.0;
-  h.gamma = live ? inv : 0.0;
-  // a > ~1e290: squares about to overflow -> poison R (reported as ArgumentError by the epilogue)
-  beta = ahi > 0x7c300000u ? __longlong_as_double(0x7ff8000000000000ll) : beta;
-  h.beta = live ? beta : pivot;
-  return h;
-}
-
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
       : "+d"(d0), "+d"(d1)
@@ -190,7 +157,7 @@ struct MmaFold {
         const double sigma = (sg0 + sg1) + (sg2 + sg3);
         double d = dl + __shfl_xor_sync(0xffffffffu, dl, 1);
         d += __shfl_xor_sync(0xffffffffu, d, 2);
-        const Reflector h = make_reflector_mma(dt[j * 9], sigma);
+        const Reflector h = make_reflector(dt[j * 9], sigma);
         const double rc = dcol[j];
         double sv = h.gamma * fma(h.u0, rc, d);
         sv = g > j ? sv : 0.0;  // finished columns keep their reflector vectors

@@ -125,6 +125,41 @@ def test_gram_kernels(ctx, oracle, m, n):
     assert np.linalg.norm(c3 - c3_ref) <= 5 * n * EPS * np.linalg.norm(x @ bm) ** 2 + 1e-300
 
 
+@pytest.mark.parametrize("m,n", [(4000, 65), (5003, 100), (9000, 128), (7001, 129), (6000, 200), (10007, 256),
+                                 (130, 128), (17, 256)])
+def test_wide_gram(ctx, sq, oracle, m, n):
+    """BASELINE config 5 (n = 128 / 256): tsmttsm has no column limit in the reference
+    (gram.cpp:113-121); the wide DMMA kernel against the oracle, host and device entry points."""
+    import torch
+    x = gaussian(m, n, seed=3 * n + m)
+    xn2 = np.linalg.norm(x) ** 2
+    c_ref = oracle.port.tsmttsm(x)
+    c = ctx.tsmttsm(x)
+    assert np.array_equal(c, c.T)
+    assert np.linalg.norm(c - c_ref) <= 5 * n * EPS * xn2
+    xd = torch.from_numpy(np.ascontiguousarray(x.T)).cuda().t()  # column-major device tensor
+    cd = ctx.tsmttsm(xd)
+    ctx.synchronize()
+    assert np.linalg.norm(cd.cpu().numpy() - c_ref) <= 5 * n * EPS * xn2
+    # unaligned leading dimension / odd row offset takes the synchronous fill path
+    big = torch.zeros((n, m + 3), dtype=torch.float64, device="cuda")
+    big[:, 1:m + 1] = xd.t()
+    cu = ctx.tsmttsm(big.t()[1:m + 1, :])
+    ctx.synchronize()
+    assert np.linalg.norm(cu.cpu().numpy() - c_ref) <= 5 * n * EPS * xn2
+    # the fused variants keep the n <= 64 limit; tsmttsm stops at 256 columns
+    with pytest.raises(sq.ArgumentError):
+        ctx.tsmRttsmR(x, np.eye(n))
+    x[m // 2, n - 1] = np.inf
+    with pytest.raises(sq.ArgumentError):
+        ctx.tsmttsm(x)
+
+
+def test_wide_gram_limit(ctx, sq):
+    with pytest.raises(sq.ArgumentError):
+        ctx.tsmttsm(gaussian(300, 257))
+
+
 @pytest.mark.parametrize("n", [1, 2, 5, 8, 17, 32, 64])
 def test_cholesky_and_eigh(ctx, oracle, n):
     a = gaussian(4 * n + 3, n, seed=n)

@@ -1,0 +1,31 @@
+"""Wide Gram (config 5) timing: python tools/time_gram_wide.py [LOG2_M]  -> ms, GB/s, executed DMMA TFLOP/s"""
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+import paper_2603_20889_b200 as sq  # noqa: E402
+
+log2m = int(sys.argv[1]) if len(sys.argv) > 1 else 24
+ctx = sq.Context(0)
+ctx.use_torch_stream()
+for n in (96, 128, 192, 256):
+    m = 1 << log2m
+    x = ctx.fill_gaussian(m, n, seed=1234)
+    for _ in range(2):
+        ctx.tsmttsm(x)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    reps = 5
+    for _ in range(reps):
+        ctx.tsmttsm(x)
+    e1.record()
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    nt = 16 * ((n + 127) // 128)
+    pairs = 136 if nt == 16 else 528
+    print(f"tsmttsm n={n:3d} m=2^{log2m} {ms:8.3f} ms  {8.0*m*n/ms/1e6:8.1f} GB/s  nominal 2mn^2 {2.0*m*n*n/ms/1e9:6.2f} TF  "
+          f"executed DMMA {2.0*m*pairs*64/ms/1e9:6.2f} TF", flush=True)
+    del x
+    torch.cuda.empty_cache()
