@@ -31,7 +31,7 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 template <int NB, int OP>
 struct GramCfg {
   static constexpr int NPAD = 8 * NB;
-  static constexpr int NW = NB >= 8 ? 6 : 8;
+  static constexpr int NW = 8;  // whole multiples of 4 warps: 6 would leave two SM sub-partitions half idle
   static constexpr int NS = (OP == OP_SOLVE && NB >= 5) ? 1 : 2;
   // streaming panel heights: P == 8 (mod 16) keeps the plain fragment pattern unpadded, P == 0
   // (mod 16) costs the transposed pattern only 4 pad rows
@@ -47,9 +47,10 @@ struct GramCfg {
   static constexpr int kWarpDoubles = NS * kStageDoubles + kVbuf + 2 * NS;  // + mbarrier slots
   static constexpr int FP = NPAD + 4;  // factor pitch: conflict-free A-fragment reads
   static constexpr int kFacDoubles = OP == OP_PLAIN ? 0 : NPAD * FP + NPAD;
-  static constexpr int kSumDoubles = NPAD * NPAD;
+  static constexpr int kSumDoubles = NPAD * NPAD;  // aliases the warp stages after the streaming loop
+  static_assert(kSumDoubles <= kWarpDoubles * NW, "the CTA sum must fit into the stage area");
   static constexpr size_t kSmemBytes =
-      sizeof(double) * (static_cast<size_t>(kWarpDoubles) * NW + kFacDoubles + kSumDoubles);
+      sizeof(double) * (static_cast<size_t>(kWarpDoubles) * NW + kFacDoubles);
   static constexpr int NPAIR = NB * (NB + 1) / 2;
   static_assert(P >= 8 && P % 8 == 0, "panel rows");
   static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
@@ -72,12 +73,11 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(vbuf + Cfg::kVbuf);
   double* fac = smem + static_cast<size_t>(NW) * Cfg::kWarpDoubles;  // NPAD x FP, then inv diag
   double* inv = fac + NPAD * FP;
-  double* csum = fac + Cfg::kFacDoubles;
+  double* csum = smem;  // reused once every warp has left the streaming loop
 
   for (int i = lane; i < NS * Cfg::kStageDoubles + Cfg::kVbuf; i += kWarp) my[i] = 0.0;
   if (lane < NS) mbar_init(bars + lane, 1);
   mbar_fence_init();
-  for (int i = threadIdx.x; i < Cfg::kSumDoubles; i += NW * kWarp) csum[i] = 0.0;
   if (OP != OP_PLAIN) {
     for (int i = threadIdx.x; i < Cfg::kFacDoubles; i += NW * kWarp) fac[i] = 0.0;
     __syncthreads();
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
         for (int j = 0; j < NPAD; ++j) y[j] = rowp[j * PP];
         // right-looking form of the same recurrence: once y_i is final, every later column takes
         // its -r_ij*y_i term (independent FMAs); per column the terms still arrive for ascending i
-        if constexpr (NB <= 6) {
+        if constexpr (NB <= 4) {
 #pragma unroll
           for (int i = 0; i < NPAD; ++i) {
             y[i] *= inv[i];
@@ -183,7 +183,8 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
 #pragma unroll
             for (int j = i + 1; j < NPAD; ++j) y[j] = fma(-fac[i + j * FP], y[i], y[j]);
           }
-        } else {  // wide rows: left-looking keeps the register pressure (spills) read-only
+        } else {  // wide rows: left-looking keeps the register pressure read-only (the right-looking
+                  // form is demoted to local memory by nvcc beyond 32 columns)
 #pragma unroll
           for (int j = 0; j < NPAD; ++j) {
             double acc0 = y[j], acc1 = 0.0;
@@ -249,6 +250,8 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
   }
 
   // ---- CTA reduction in fixed warp order, then the block's upper-triangle partial -------------
+  __syncthreads();  // all stages drained: the stage area becomes the CTA sum
+  for (int i = threadIdx.x; i < Cfg::kSumDoubles; i += NW * kWarp) csum[i] = 0.0;
   for (int wi = 0; wi < NW; ++wi) {
     __syncthreads();
     if (warp == wi) {
@@ -351,7 +354,7 @@ int gram_panel_rows(int n, int op) {
 
 int gram_warps(int n) {
   if (n <= kThreadGramMaxN) return gram_thread_warps();
-  return (n + 7) / 8 >= 8 ? 6 : 8;
+  return 8;
 }
 
 int gram_ctas_per_sm(int n, int op) { return n <= kThreadGramMaxN ? gram_thread_ctas_per_sm(n, op) : 1; }
