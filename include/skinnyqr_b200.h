@@ -89,13 +89,14 @@ int sqb_block_qless_qr_dev(sqb_context* ctx, const double* d_x, int64_t m, int64
                            int64_t ld, int64_t panel_rows, double* d_r);
 
 /* ---- Gram kernels (include/skinnyqr/gram.hpp:12-21, src/gram.cpp:113-151) ----------------- */
-/* C = X^T X                                                  (tsmttsm)                     */
+/* C = X^T X (tsmttsm); n <= 256: the reference has no column limit here, 65..256 columns run
+ * the wide FP64 tensor-core kernel and ignore num_blocks / panel_rows (BASELINE config 5)   */
 int sqb_tsmttsm_dev(sqb_context* ctx, const double* d_x, int64_t m, int64_t n, int64_t ld,
                     int64_t num_blocks, int64_t panel_rows, double* d_c);
-/* C = (X R^-1)^T (X R^-1), R upper triangular n x n on device (tsmRttsmR)                  */
+/* C = (X R^-1)^T (X R^-1), R upper triangular n x n on device (tsmRttsmR); n <= 64        */
 int sqb_tsmRttsmR_dev(sqb_context* ctx, const double* d_x, int64_t m, int64_t n, int64_t ld,
                       const double* d_r, int64_t num_blocks, int64_t panel_rows, double* d_c);
-/* C = (X B)^T (X B), B dense n x n on device                 (tsmmttsmm)                   */
+/* C = (X B)^T (X B), B dense n x n on device                 (tsmmttsmm); n <= 64          */
 int sqb_tsmmttsmm_dev(sqb_context* ctx, const double* d_x, int64_t m, int64_t n, int64_t ld,
                       const double* d_b, int64_t num_blocks, int64_t panel_rows, double* d_c);
 

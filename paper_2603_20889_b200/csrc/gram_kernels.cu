@@ -32,21 +32,26 @@ template <int NB, int OP>
 struct GramCfg {
   static constexpr int NPAD = 8 * NB;
   static constexpr int NW = 8;  // whole multiples of 4 warps: 6 would leave two SM sub-partitions half idle
-  static constexpr int NS = (OP == OP_SOLVE && NB >= 5) ? 1 : 2;
+  static constexpr int NS = 2;
+  // OP_SOLVE beyond 32 columns: blocked substitution on the tensor cores (8 x 8 diagonal blocks by
+  // their explicit inverses, everything off the diagonal as DMMA updates) instead of lane = row
+  static constexpr bool kBlockedSolve = OP == OP_SOLVE && NB >= 5;
   // streaming panel heights: P == 8 (mod 16) keeps the plain fragment pattern unpadded, P == 0
   // (mod 16) costs the transposed pattern only 4 pad rows
   static constexpr int kPlainP[8] = {120, 72, 40, 40, 24, 24, 24, 24};
   static constexpr int kMultP[8] = {112, 64, 48, 32, 32, 16, 16, 16};
   // OP_SOLVE: one lane substitutes one row, so the panel height is a multiple of 32
-  static constexpr int kSolveP[8] = {64, 64, 32, 32, 32, 32, 32, 32};
+  static constexpr int kSolveP[8] = {64, 64, 32, 32, 16, 16, 16, 16};
   static constexpr int P =
       OP == OP_SOLVE ? kSolveP[NB - 1] : (OP == OP_PLAIN ? kPlainP[NB - 1] : kMultP[NB - 1]);
-  static constexpr int PP = stage_pitch(P, OP == OP_MULTIPLY ? 4 : 8);
+  static constexpr int PP = stage_pitch(P, (OP == OP_MULTIPLY || kBlockedSolve) ? 4 : 8);
   static constexpr int kStageDoubles = NPAD * PP;
   static constexpr int kVbuf = 0;
   static constexpr int kWarpDoubles = NS * kStageDoubles + kVbuf + 2 * NS;  // + mbarrier slots
   static constexpr int FP = NPAD + 4;  // factor pitch: conflict-free A-fragment reads
-  static constexpr int kFacDoubles = OP == OP_PLAIN ? 0 : NPAD * FP + NPAD;
+  static constexpr int kDinvPitch = 12;  // (4k+q) + 12 g: conflict-free A-fragment reads of an 8 x 8 block
+  static constexpr int kFacDoubles =
+      OP == OP_PLAIN ? 0 : NPAD * FP + NPAD + (kBlockedSolve ? NB * 8 * kDinvPitch : 0);
   static constexpr int kSumDoubles = NPAD * NPAD;  // aliases the warp stages after the streaming loop
   static_assert(kSumDoubles <= kWarpDoubles * NW, "the CTA sum must fit into the stage area");
   static constexpr size_t kSmemBytes =
@@ -86,6 +91,27 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
       if (OP == OP_MULTIPLY || r <= c) fac[r + c * FP] = prm.factor[i];
     }
     __syncthreads();
+    if constexpr (Cfg::kBlockedSolve) {
+      // explicit inverses of the 8 x 8 diagonal blocks (thread = one column of one block, back
+      // substitution; padded columns act as identity), then the strictly upper blocks are negated
+      // so that the DMMA updates subtract
+      double* dinv = inv + NPAD;
+      if (threadIdx.x < NPAD) {
+        const int b = threadIdx.x >> 3, j = threadIdx.x & 7;
+        double xcol[8];
+#pragma unroll
+        for (int i = 7; i >= 0; --i) {
+          double v = i == j ? 1.0 : 0.0;
+#pragma unroll
+          for (int k2 = i + 1; k2 < 8; ++k2)
+            if (k2 <= j) v = fma(-fac[(8 * b + i) + (8 * b + k2) * FP], xcol[k2], v);
+          const double dgn = (8 * b + i) < n ? fac[(8 * b + i) + (8 * b + i) * FP] : 1.0;
+          xcol[i] = i <= j ? v / dgn : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dinv[b * 8 * Cfg::kDinvPitch + i + Cfg::kDinvPitch * j] = xcol[i];
+      }
+    }
     if (OP == OP_SOLVE) {
       // reference tsmRttsmR pre-check (gram.cpp:126-134): |r_jj| > n*eps*max|r_jj|, else
       // SingularFactorError(j) for the first offending j; inv_diag precomputed.
@@ -100,6 +126,13 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
           inv[j] = 1.0 / d;
         }
         if (bad >= 0 && blockIdx.x == 0) raise_status(prm.status, SQB_E_SINGULAR, bad);
+      }
+    }
+    if constexpr (Cfg::kBlockedSolve) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < NPAD * NPAD; i += NW * kWarp) {
+        const int r = i % NPAD, c = i / NPAD;
+        if ((r >> 3) < (c >> 3)) fac[r + c * FP] = -fac[r + c * FP];
       }
     }
   }
@@ -159,6 +192,56 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
         for (int b = 0; b < NB; ++b)
 #pragma unroll
           for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], a[b].y, a[b2].y);
+      }
+      __syncwarp();
+      if (pnl + static_cast<long long>(NS) * NW < npanels) issue(pnl + static_cast<long long>(NS) * NW, s);
+    } else if (Cfg::kBlockedSolve) {
+      // Y = X R^-1 by 8-column blocks, 8 rows at a time, transposed so that the result lands in the
+      // Gram fragment layout: Y_b^T = Rbb^-T (X_b^T - sum_{a<b} R_ab^T Y_a^T).  Finished blocks are
+      // written back to the stage, where later blocks read them as B fragments (row g, column 4k+q).
+      double* wstage = my + s * Cfg::kStageDoubles;
+      const double* dinv = inv + NPAD;
+#pragma unroll 1
+      for (int t = 0; t < P / 8; ++t) {
+        double2 y[NB];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          double* own = wstage + (8 * b + g) * PP + 8 * t + 2 * q;
+          const double2 x2 = *reinterpret_cast<const double2*>(own);
+          double z0 = x2.x, z1 = x2.y;
+#pragma unroll
+          for (int a = 0; a < b; ++a) {
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+              const double af = fac[(8 * a + 4 * kk + q) + (8 * b + g) * FP];  // -R_ab
+              const double bf = wstage[(8 * a + 4 * kk + q) * PP + 8 * t + g];
+              dmma884(z0, z1, af, bf);
+            }
+          }
+          *reinterpret_cast<double2*>(own) = make_double2(z0, z1);
+          __syncwarp();
+          double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            const double af = dinv[b * 8 * Cfg::kDinvPitch + (4 * kk + q) + Cfg::kDinvPitch * g];
+            const double bf = wstage[(8 * b + 4 * kk + q) * PP + 8 * t + g];
+            dmma884(w0, w1, af, bf);
+          }
+          __syncwarp();  // every lane has read Z_b before Y_b replaces it
+          *reinterpret_cast<double2*>(own) = make_double2(w0, w1);
+          __syncwarp();
+          y[b] = make_double2(w0, w1);
+        }
+        int p = 0;
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+          for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], y[b].x, y[b2].x);
+        p = 0;
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+          for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], y[b].y, y[b2].y);
       }
       __syncwarp();
       if (pnl + static_cast<long long>(NS) * NW < npanels) issue(pnl + static_cast<long long>(NS) * NW, s);

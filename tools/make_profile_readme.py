@@ -1,0 +1,173 @@
+"""Builds profiles/README.md and copies the round's evidence from gpurun_out/ into profiles/.
+python tools/make_profile_readme.py [tag]"""
+import csv
+import json
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+G, P = ROOT / "gpurun_out", ROOT / "profiles"
+tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+P.mkdir(exist_ok=True)
+
+
+def jline(path):
+    for line in open(path):
+        line = line.strip()
+        if line.startswith("{"):
+            return json.loads(line)
+    return None
+
+
+out = [f"# Round evidence ({tag}) - one B200, sm_100a\n",
+       "Everything here was produced by `tools/round_profile.sh` under `gpurun` (one command, one box): "
+       "`bench.py` for both arms, the ncu launch list of the same bench command, one `ncu --set full` capture per "
+       "streaming kernel family (kept as raw-metric CSVs: the `.ncu-rep` files together exceed what gpurun returns), "
+       "the `nvidia-smi` clock log during the bench, and the BASELINE configurations C1/C3/C4/C5 (`tools/run_configs.py`). "
+       "Numbers under ncu are cold-cache and serialised: compare shares, not absolutes.\n"]
+
+bench = jline(G / f"{tag}_bench.json")
+ref = jline(G / f"{tag}_bench_reference.json")
+if bench:
+    shutil.copy(G / f"{tag}_bench.json", P / f"{tag}_bench.json")
+    r = bench["roofline"]
+    out.append("## Headline (bench.py, N = 1)\n")
+    out.append(f"* workload: {bench['config']['workload']}; plan {bench['config']['plan']}")
+    out.append(f"* **value {bench['value']:.0f} GB/s** ({bench['ms_per_step']:.3f} ms per step, {bench['gpu_launches']} launches in the timed region), "
+               f"{100*bench['value']/8000:.1f} % of the nominal 8 TB/s roofline, {100*bench['value']/r['peak']:.1f} % of the measured copy bandwidth ({r['peak']:.0f} GB/s); "
+               f"clocks {bench['clocks']}")
+    if "sustained" in bench:
+        s = bench["sustained"]
+        out.append(f"* sustained (after 300 ms of back-to-back steps): {s['value']:.0f} GB/s, clocks {s['clocks']}")
+    out.append(f"* roofline (stage-1 kernel alone, in situ): achieved {r['achieved']:.0f} GB/s = {r['frac']:.3f} of measured peak; "
+               f"DRAM traffic per launch {r['traffic']} B vs algorithmic {r['algorithmic_bytes_per_launch']:.0f} B")
+    if "e2e" in bench:
+        e = bench["e2e"]
+        out.append(f"* e2e through the host-pointer ABI: {e['value']:.1f} GB/s ({e['ms_per_step']:.1f} ms per step, H2D {e['h2d_bytes_per_step']} B per step inside the timed region: PCIe-bound)")
+    if "cpu_baseline" in bench:
+        c = bench["cpu_baseline"]
+        out.append(f"* CPU reference beside it: {c.get('value', 0):.2f} GB/s on {c.get('cores')} host threads ({c.get('kernel_table')}), "
+                   f"{c.get('value_without_validation_scan', 0):.1f} GB/s without its serial validation scan; sample: {c.get('sample')}")
+    if "parity" in bench:
+        out.append(f"* parity of the headline run against the reference on that sample: {bench['parity']}")
+    if ref:
+        out.append(f"* `bench.py --impl reference`: {ref['value']:.2f} GB/s ({ref['cpu_baseline']['sample']})")
+    if "sweep" in bench:
+        out.append("\n## Column sweep at m = 2^27 (BASELINE configs[1]); ms / effective GB/s (8mn / t) / % of 8 TB/s\n")
+        out.append("| n | GiB | TSQR | CholQR2 | SVQB2 | TSQR TFLOP/s (2mn^2) |")
+        out.append("|---|---|---|---|---|---|")
+        for row in bench["sweep"]:
+            cells = []
+            for meth in ("tsqr", "cholqr2", "svqb2"):
+                v = row.get(meth, {})
+                cells.append(f"{v['ms']:.2f} ms / {v['gbs']:.0f} / {100*v['frac_8TBs']:.1f} %" if "ms" in v else str(v))
+            out.append(f"| {row['n']} | {row['gib']:.0f} | {cells[0]} | {cells[1]} | {cells[2]} | {row['tsqr'].get('fp64_tflops_2mn2', 0):.1f} |")
+
+# launch list
+lf = G / f"{tag}_launches.csv"
+if lf.exists():
+    shutil.copy(lf, P / f"{tag}_launches.csv")
+    rows = [r for r in csv.reader(l for l in open(lf) if not l.startswith("==")) if len(r) > 5]
+    hdr = rows[0]
+    if "Kernel Name" in hdr:
+        kn, mv = hdr.index("Kernel Name"), hdr.index("Metric Value")
+        agg = {}
+        for r in rows[1:]:
+            try:
+                t = float(r[mv].replace(",", ""))
+            except ValueError:
+                continue
+            name = r[kn].split("(")[0].replace("void ", "").replace("sqb::", "").replace("<unnamed>::", "")
+            a = agg.setdefault(name, [0, 0.0])
+            a[0] += 1
+            a[1] += t
+        tot = sum(v[1] for v in agg.values())
+        out.append(f"\n## Launch list of `bench.py --steps 2 --warmup 1` under ncu ({tag}_launches.csv), share of device time\n")
+        out.append("| kernel | launches | total | share |")
+        out.append("|---|---|---|---|")
+        for name, (cnt, t) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:16]:
+            out.append(f"| `{name}` | {cnt} | {t/1e6:.2f} ms | {100*t/tot:.1f} % |")
+
+# ncu summaries
+raws = sorted(G.glob(f"{tag}_*.raw.csv"))
+if raws:
+    txt = subprocess.run([sys.executable, str(ROOT / "tools" / "ncu_summary_csv.py")] + [str(r) for r in raws],
+                         capture_output=True, text=True).stdout
+    (P / f"{tag}_ncu_summary.txt").write_text(txt)
+    for r in raws:
+        shutil.copy(r, P / r.name)
+    for r in G.glob(f"{tag}_*.source.csv"):
+        shutil.copy(r, P / r.name)
+    out.append(f"\n## ncu --set full, one capture per kernel family ({tag}_ncu_summary.txt, raw CSVs beside it)\n")
+    out.append("```")
+    out.append(txt.replace(str(G) + "/", ""))
+    out.append("```")
+    # traffic.json for bench.py
+    traffic = {}
+    for r in raws:
+        rows = list(csv.reader(open(r)))
+        if len(rows) < 3:
+            continue
+        hdr = rows[0]
+        try:
+            rd = float(rows[2][hdr.index("dram__bytes_read.sum")])
+            wr = float(rows[2][hdr.index("dram__bytes_write.sum")])
+            ur, uw = rows[1][hdr.index("dram__bytes_read.sum")], rows[1][hdr.index("dram__bytes_write.sum")]
+        except (ValueError, IndexError):
+            continue
+        mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        traffic[r.name.replace(f"{tag}_", "").replace(".raw.csv", "")] = rd * mult.get(ur, 1) + wr * mult.get(uw, 1)
+    t8 = traffic.get("tsqr_thread_n8")
+    tj = {"_source": f"profiles/{tag}_*.raw.csv (ncu --set full): dram__bytes_read.sum + dram__bytes_write.sum per launch", "all": traffic}
+    if t8:
+        tj["tsqr_n8"] = t8
+    (P / "traffic.json").write_text(json.dumps(tj, indent=1))
+
+cf = G / f"configs_{tag}.json"
+if cf.exists():
+    shutil.copy(cf, P / f"{tag}_configs.json")
+    c = json.loads(cf.read_text())
+    out.append(f"\n## BASELINE configurations ({tag}_configs.json)\n")
+    if "C1" in c:
+        out.append("**C1** 1 000 000 x 8 Gaussian, GPU resident / host API / CPU reference (ms), error against the reference's R (bound 64 n eps |X|):\n")
+        for meth in ("tsqr", "cholqr2"):
+            v = c["C1"][meth]
+            out.append(f"* {meth}: {v['gpu_ms_resident']:.3f} / {v['gpu_ms_host_api']:.2f} / {v['cpu_reference_ms']:.1f} ms; err {v['err_vs_reference_tsqr']:.2e} (bound {v['bound']:.2e})")
+        v = c["C1"]["svqb2"]
+        out.append(f"* svqb2: {v['gpu_ms_resident']:.3f} ms resident, CPU {v['cpu_reference_ms']:.1f} ms, rank {v['rank']}, sigma rel err {v['sigma_rel_err']:.1e}")
+    if "C3" in c:
+        out.append("\n**C3** 4e7 x 32, controlled condition number (device-side restatement of the reference generator):\n")
+        out.append("| kappa | TSQR ms | TSQR |R-R_ref| (bound) | TSQR orth loss | CholQR2 | SVQB2 | CPU ref cholqr2 |")
+        out.append("|---|---|---|---|---|---|---|")
+        for r in c["C3"]:
+            ch = f"{r['cholqr2_ms']:.2f} ms, err vs TSQR {r['cholqr2_err_vs_tsqr']:.1e}, orth {r['cholqr2_orth_loss_2norm']:.1e}" if "cholqr2_ms" in r else r.get("cholqr2")
+            sv = f"{r['svqb2_ms']:.2f} ms, rank {r['svqb2_rank']}" if "svqb2_ms" in r else r.get("svqb2")
+            out.append(f"| {r['kappa']:.0e} | {r['tsqr_ms']:.2f} | {r['tsqr_err_vs_reference']:.1e} ({r['bound_64_n_eps_normX']:.1e}) | {r['tsqr_orth_loss_2norm']:.1e} | {ch} | {sv} | {r['cpu_reference_cholqr2']} (ref svqb2 rank {r['cpu_reference_svqb2_rank']}) |")
+    if "C4" in c:
+        v = c["C4"]
+        out.append(f"\n**C4** least squares, {v['m']} x {v['n_A']} + rhs on one GPU ({v['bytes']/1e9:.0f} GB streamed once): "
+                   + "; ".join(f"{m_}: {v[m_]['ms']:.1f} ms = {v[m_]['gbs']:.0f} GB/s, max |x - planted| {v[m_]['max_abs_err_vs_planted']:.1e}" for m_ in ("tsqr", "cholqr2"))
+                   + f"; parity vs CPU reference at 1e7 rows {v['parity_vs_cpu_reference_at_1e7_rows']:.1e}")
+    if "C5" in c:
+        out.append("\n**C5** Gram matrix at m = 2^24 on the FP64 tensor cores (executed DMMA flops count whole 8x8 tiles of the upper triangle):\n")
+        out.append("| n | tsmttsm ms | GB/s | nominal TFLOP/s (2mn^2) | executed DMMA TFLOP/s | DMMA pipe use vs 37.1 | parity err (bound) | TSQR beside it |")
+        out.append("|---|---|---|---|---|---|---|---|")
+        for r in c["C5"]:
+            ts = f"{r['tsqr_ms']:.1f} ms = {r['tsqr_tflops_2mn2']:.1f} TFLOP/s" if "tsqr_ms" in r else "reference rejects n > 64"
+            out.append(f"| {r['n']} | {r['tsmttsm_ms']:.2f} | {r['gbs']:.0f} | {r['nominal_tflops_2mn2']:.1f} | {r['executed_dmma_tflops']:.1f} | {100*r['dmma_pipe_util_vs_37.1']:.0f} % | {r['parity_err_F_at_2^17_rows']:.1e} ({r['parity_bound_5_n_eps_normX2']:.1e}) | {ts} |")
+
+clk = G / f"{tag}_clocks.csv"
+if clk.exists():
+    shutil.copy(clk, P / f"{tag}_clocks.csv")
+    rows = list(csv.reader(open(clk)))[1:]
+    sm = sorted(int(r[1].split()[0]) for r in rows if len(r) > 3 and r[1].split()[0].isdigit())
+    reasons = sorted({r[4].strip() for r in rows if len(r) > 4})
+    if sm:
+        out.append(f"\n## Clocks during the bench ({tag}_clocks.csv)\n\nSM clock min/median/max {sm[0]}/{sm[len(sm)//2]}/{sm[-1]} MHz over {len(sm)} samples; active reasons seen: {reasons}")
+tests = G / f"{tag}_gpu_tests.txt"
+if tests.exists():
+    out.append(f"\n## GPU tests on the same box\n\n```\n{tests.read_text().strip()}\n```")
+(P / "README.md").write_text("\n".join(out) + "\n")
+print("wrote", P / "README.md")

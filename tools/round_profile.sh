@@ -1,0 +1,36 @@
+#!/bin/bash
+# Everything the round's evidence needs, on one B200: bench (both arms), launch list, full ncu captures
+# of every streaming kernel family, clocks during the bench, BASELINE configs C1/C3/C4/C5.
+set -x
+TAG=${1:-r01}
+python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/${TAG}_gpu_tests.txt
+O=gpurun_out
+mkdir -p $O
+nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap --format=csv -lms 200 > $O/${TAG}_clocks.csv &
+SMI=$!
+python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err
+kill $SMI
+python bench.py --impl reference --steps 5 --warmup 1 > $O/${TAG}_bench_reference.json 2>> $O/${TAG}_bench.err
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --sweep-reps 1 > $O/${TAG}_bench_under_ncu.log 2>&1
+prof() { # name kernel-regex method n log2m : full capture, kept as the raw-metrics CSV (the .ncu-rep files
+         # together exceed what gpurun brings back); the source page is kept for the headline kernels
+  ncu --set full --clock-control none --import-source on -k regex:$2 -c 1 -o $O/${TAG}_$1 python tools/prof_run.py $3 $4 $5 1 > /dev/null 2>&1
+  ncu -i $O/${TAG}_$1.ncu-rep --page raw --csv > $O/${TAG}_$1.raw.csv 2>/dev/null
+  case $1 in tsqr_thread_n8|tsqr_fold_n16|tsqr_mma_n32) ncu -i $O/${TAG}_$1.ncu-rep --page source --csv > $O/${TAG}_$1.source.csv 2>/dev/null;; esac
+  rm -f $O/${TAG}_$1.ncu-rep
+}
+prof tsqr_thread_n8 tsqr_thread stage1 8 27
+prof tsqr_thread_n4 tsqr_thread stage1 4 27
+prof tsqr_fold_n12 tsqr_fold stage1 12 27
+prof tsqr_fold_n16 tsqr_fold stage1 16 27
+prof tsqr_fold_n24 tsqr_fold stage1 24 26
+prof tsqr_mma_n32 tsqr_mma stage1 32 26
+prof tsqr_mma_n64 tsqr_mma stage1 64 25
+prof gram_thread_n8 gram_thread tsmttsm 8 27
+prof gram_mma_n16 gram_mma tsmttsm 16 27
+prof gram_mma_n32 gram_mma tsmttsm 32 26
+prof gram_mma_n64 gram_mma tsmttsm 64 25
+prof gram_wide_n128 gram_wide_kernel tsmttsm 128 23
+prof gram_wide_n256 gram_wide_kernel tsmttsm 256 22
+python tools/run_configs.py $TAG > $O/${TAG}_configs.log 2>&1
+ls -la $O

@@ -163,6 +163,42 @@ c4["parity_vs_cpu_reference_at_1e7_rows"] = float(np.abs(xs_gpu.cpu().numpy() - 
 out["C4"] = c4
 print("C4", json.dumps(c4), flush=True)
 
+del a, rhs
+torch.cuda.empty_cache()
+
+# ---- C5 ----------------------------------------------------------------------------------------
+# transitional regime: the Gram matrix of a 2^24 x n matrix, n = 128 / 256, on the FP64 tensor cores.
+# The reference's tsqr_qless rejects n > 64 (tsqr.cpp:188), so there is no TSQR arm at these widths;
+# the widest TSQR (n = 64) is timed beside it for the flop-rate comparison.
+m = (1 << 20) if small else (1 << 24)
+c5 = []
+for n in (64, 128, 256):
+    x = ctx.fill_gaussian(m, n, seed=1234)
+    row = {"m": m, "n": n}
+    ms = gpu_ms(lambda: ctx.tsmttsm(x), 5, 2)
+    tiles = (n + 7) // 8 if n <= 64 else 16 * ((n + 127) // 128)
+    pairs = tiles * (tiles + 1) // 2
+    row["tsmttsm_ms"] = ms
+    row["gbs"] = 8.0 * m * n / ms / 1e6
+    row["nominal_tflops_2mn2"] = 2.0 * m * n * n / ms / 1e9
+    row["executed_dmma_tflops"] = 2.0 * m * pairs * 64 / ms / 1e9
+    row["dmma_pipe_util_vs_37.1"] = row["executed_dmma_tflops"] / 37.1
+    mc = 1 << 17
+    xh = np.asfortranarray(x[:mc].cpu().numpy())
+    c_gpu = ctx.tsmttsm(x[:mc])
+    ctx.synchronize()
+    c_ref = ref.tsmttsm(xh)
+    row["parity_err_F_at_2^17_rows"] = float(np.linalg.norm(c_gpu.cpu().numpy() - c_ref))
+    row["parity_bound_5_n_eps_normX2"] = float(5 * n * EPS * np.linalg.norm(xh) ** 2)
+    if n <= 64:
+        row["tsqr_ms"] = gpu_ms(lambda: ctx.tsqr_qless(x), 3, 1)
+        row["tsqr_tflops_2mn2"] = 2.0 * m * n * n / row["tsqr_ms"] / 1e9
+    c5.append(row)
+    print("C5", json.dumps(row), flush=True)
+    del x
+    torch.cuda.empty_cache()
+out["C5"] = c5
+
 dst = ROOT / "gpurun_out" / f"configs_{tag}.json"
 dst.parent.mkdir(exist_ok=True)
 dst.write_text(json.dumps(out, indent=1))
