@@ -25,8 +25,11 @@ namespace {
 
 constexpr int kWT = 16;          // tiles per chunk side
 constexpr int kWC = 8 * kWT;     // columns per chunk (128)
-constexpr int kWP = 16;          // panel rows
-constexpr int kWPP = 24;         // stage pitch == 8 (mod 16): conflict-free LDS.128 fragment reads
+// panel rows == stage pitch == 8 (mod 16): conflict-free LDS.128 fragment reads without padding.  The
+// triangular chunk stages 128 columns, the full one 256, so the former affords taller panels (fewer
+// CTA barriers per row) in the same shared memory.
+constexpr int kTriP = 40;
+constexpr int kFullP = 24;
 constexpr int kWThreads = 256;   // 8 warps
 constexpr int kWStages = 4;      // panels in flight (HBM latency is ~2 panel times)
 
@@ -45,8 +48,9 @@ struct WideParams {
   double* partial;      // one 128 x 128 column-major slab per CTA
 };
 
+template <int PP>
 __device__ __forceinline__ double2 frag(const double* stage, int tile, int t, int g, int q) {
-  return *reinterpret_cast<const double2*>(stage + (8 * tile + g) * kWPP + 8 * t + 2 * q);
+  return *reinterpret_cast<const double2*>(stage + (8 * tile + g) * PP + 8 * t + 2 * q);
 }
 
 // Triangular chunk, warp W: tile rows W and 15-W of the 16 x 16 upper block triangle.
@@ -54,10 +58,10 @@ template <int W>
 __device__ __forceinline__ void tri_panel(const double* stage, double (&acc)[32][2], int g, int q) {
   constexpr int R1 = W, R2 = kWT - 1 - W;
 #pragma unroll
-  for (int t = 0; t < kWP / 8; ++t) {
+  for (int t = 0; t < kTriP / 8; ++t) {
     double2 b[kWT - R1];
 #pragma unroll
-    for (int j = R1; j < kWT; ++j) b[j - R1] = frag(stage, j, t, g, q);
+    for (int j = R1; j < kWT; ++j) b[j - R1] = frag<kTriP>(stage, j, t, g, q);
     const double2 a1 = b[0], a2 = b[R2 - R1];
 #pragma unroll
     for (int j = R1; j < kWT; ++j) dmma_w(acc[j - R1][0], acc[j - R1][1], a1.x, b[j - R1].x);
@@ -74,11 +78,11 @@ __device__ __forceinline__ void tri_panel(const double* stage, double (&acc)[32]
 // the J chunk (stage slots 128..255).
 __device__ __forceinline__ void full_panel(const double* stage, double (&acc)[32][2], int w, int g, int q) {
 #pragma unroll
-  for (int t = 0; t < kWP / 8; ++t) {
-    const double2 a1 = frag(stage, 2 * w, t, g, q), a2 = frag(stage, 2 * w + 1, t, g, q);
+  for (int t = 0; t < kFullP / 8; ++t) {
+    const double2 a1 = frag<kFullP>(stage, 2 * w, t, g, q), a2 = frag<kFullP>(stage, 2 * w + 1, t, g, q);
     double2 b[kWT];
 #pragma unroll
-    for (int j = 0; j < kWT; ++j) b[j] = frag(stage, kWT + j, t, g, q);
+    for (int j = 0; j < kWT; ++j) b[j] = frag<kFullP>(stage, kWT + j, t, g, q);
 #pragma unroll
     for (int j = 0; j < kWT; ++j) dmma_w(acc[j][0], acc[j][1], a1.x, b[j].x);
 #pragma unroll
@@ -136,6 +140,7 @@ __global__ void __launch_bounds__(kWThreads, 1) gram_wide_kernel(const WideParam
   }
   const bool tri = ci == cj;
   const int nslots = tri ? kWC : 2 * kWC;
+  const int kWP = tri ? kTriP : kFullP, kWPP = kWP;  // panel rows and stage pitch of this chunk type
   const int stage_doubles = nslots * kWPP;
 
   // column of this thread's stage slot (every thread copies one column segment per panel)
@@ -280,11 +285,11 @@ cudaError_t launch_gram_wide(const double* x, long long m, int n, long long ld, 
     prm.kb_tri = (sm_count - prm.kb_full) / 2;
     grid = 2 * prm.kb_tri + prm.kb_full;
   }
-  const long long panels = (m + kWP - 1) / kWP;
+  const long long panels = (m + kTriP - 1) / kTriP;
   if (prm.kb_tri > panels) prm.kb_tri = static_cast<int>(panels > 0 ? panels : 1);
   if (prm.kb_full > panels) prm.kb_full = static_cast<int>(panels > 0 ? panels : 1);
   if (prm.nchunk == 1) grid = prm.kb_tri; else grid = 2 * prm.kb_tri + prm.kb_full;
-  const size_t bytes = sizeof(double) * kWStages * (2 * kWC) * kWPP;
+  const size_t bytes = sizeof(double) * kWStages * (kWC * kTriP > 2 * kWC * kFullP ? kWC * kTriP : 2 * kWC * kFullP);
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(gram_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

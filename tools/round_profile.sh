@@ -11,7 +11,7 @@ SMI=$!
 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err
 kill $SMI
 python bench.py --impl reference --steps 5 --warmup 1 > $O/${TAG}_bench_reference.json 2>> $O/${TAG}_bench.err
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --sweep-reps 1 > $O/${TAG}_bench_under_ncu.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-sweep > $O/${TAG}_bench_under_ncu.log 2>&1
 prof() { # name kernel-regex method n log2m : full capture, kept as the raw-metrics CSV (the .ncu-rep files
          # together exceed what gpurun brings back); the source page is kept for the headline kernels
   ncu --set full --clock-control none --import-source on -k regex:$2 -c 1 -o $O/${TAG}_$1 python tools/prof_run.py $3 $4 $5 1 > /dev/null 2>&1
