@@ -35,8 +35,8 @@ cudaError_t launch_tsqr_group(const TsqrParams& prm, long long num_blocks, cudaS
 int tsqr_group_chunk_rows(int n);
 int tsqr_group_warps(int n);
 
-// ---- tsqr_fold_kernels.cu (8 < n <= 64: lookahead lane-group kernel with retire loads) --------
-constexpr int kFoldTsqrMinN = 9;
+// ---- tsqr_fold_kernels.cu (5 <= n <= 64: lookahead lane-group kernel with retire loads) -------
+constexpr int kFoldTsqrMinN = 5;
 cudaError_t launch_tsqr_fold(const TsqrParams& prm, long long num_blocks, cudaStream_t stream);
 int tsqr_fold_chunk_rows(int n);
 int tsqr_fold_warps(int n);
@@ -48,7 +48,7 @@ int tsqr_mma_panel_rows(int n);
 int tsqr_mma_warps(int n);
 
 // Kernel selection by column count (measured on B200, profiles/README.md): register-resident thread
-// kernel up to 8 columns, lookahead fold kernel for 9..28, DMMA blocked kernel for 29..64.
+// kernel up to 4 columns, lookahead fold kernel for 5..28, DMMA blocked kernel for 29..64.
 // SQB_TSQR_KERNEL=0..4 forces thread / lane-group / warp-panel / fold / DMMA where the column count
 // allows it (tuning, A/B tests and the kernel-family parity test only).
 int tsqr_forced_kind();
@@ -65,7 +65,7 @@ inline int tsqr_kernel_kind(int n) {
     if (n <= 32) return 2;
     return 1;
   }
-  if (n <= 8) return 0;
+  if (n < kFoldTsqrMinN) return 0;
   if (n <= 28) return 3;
   return 4;
 }

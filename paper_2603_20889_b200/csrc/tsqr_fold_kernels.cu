@@ -1,4 +1,4 @@
-// Lookahead lane-group Q-less Householder TSQR, 8 < n <= 64  ("fold" kernels).
+// Lookahead lane-group Q-less Householder TSQR, 5 <= n <= 64  ("fold" kernels).
 //
 // Reference semantics: block_qless_qr_core / factor_trapezoidal / make_reflector
 // (reference src/tsqr.cpp:51-158): fold row panels into a running upper triangle with Householder
@@ -328,11 +328,16 @@ cudaError_t launch_cfg(const TsqrParams& prm, long long num_blocks, cudaStream_t
 }  // namespace
 
 // column count -> (slots per lane, lanes per group, rows per step, max threads per CTA); measured
-// on B200 (gpurun_out/fold_select.txt, profiles/README.md): thread-private leaves up to 14 columns,
+// on B200 (gpurun_out/fold_select.txt, profiles/README.md): thread-private leaves up to 14 columns
+// (5..8 columns: taller steps than the register-triangle kernel, 5-9 % faster under the power cap),
 // lane pairs up to 20, lane quads up to 28; above that the DMMA kernel (tsqr_mma_kernels.cu) wins
 // and the last three rows only serve SQB_TSQR_KERNEL=3
 #define SQB_FOLD_SWITCH(EXPR)                 \
   switch (n) {                                \
+    case 5: return EXPR(5, 1, 16, 256);       \
+    case 6: return EXPR(6, 1, 16, 256);       \
+    case 7: return EXPR(7, 1, 12, 256);       \
+    case 8: return EXPR(8, 1, 12, 256);       \
     case 9: return EXPR(9, 1, 8, 256);        \
     case 10: return EXPR(10, 1, 8, 256);      \
     case 11: return EXPR(11, 1, 8, 256);      \

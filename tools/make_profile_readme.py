@@ -119,7 +119,7 @@ if raws:
             continue
         mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         traffic[r.name.replace(f"{tag}_", "").replace(".raw.csv", "")] = rd * mult.get(ur, 1) + wr * mult.get(uw, 1)
-    t8 = traffic.get("tsqr_thread_n8")
+    t8 = traffic.get("tsqr_fold_n8")
     tj = {"_source": f"profiles/{tag}_*.raw.csv (ncu --set full): dram__bytes_read.sum + dram__bytes_write.sum per launch", "all": traffic}
     if t8:
         tj["tsqr_n8"] = t8

@@ -16,10 +16,10 @@ prof() { # name kernel-regex method n log2m : full capture, kept as the raw-metr
          # together exceed what gpurun brings back); the source page is kept for the headline kernels
   ncu --set full --clock-control none --import-source on -k regex:$2 -c 1 -o $O/${TAG}_$1 python tools/prof_run.py $3 $4 $5 1 > /dev/null 2>&1
   ncu -i $O/${TAG}_$1.ncu-rep --page raw --csv > $O/${TAG}_$1.raw.csv 2>/dev/null
-  case $1 in tsqr_thread_n8|tsqr_fold_n16|tsqr_mma_n32) ncu -i $O/${TAG}_$1.ncu-rep --page source --csv > $O/${TAG}_$1.source.csv 2>/dev/null;; esac
+  case $1 in tsqr_fold_n8|tsqr_fold_n16|tsqr_mma_n32) ncu -i $O/${TAG}_$1.ncu-rep --page source --csv > $O/${TAG}_$1.source.csv 2>/dev/null;; esac
   rm -f $O/${TAG}_$1.ncu-rep
 }
-prof tsqr_thread_n8 tsqr_thread stage1 8 27
+prof tsqr_fold_n8 tsqr_fold stage1 8 27
 prof tsqr_thread_n4 tsqr_thread stage1 4 27
 prof tsqr_fold_n12 tsqr_fold stage1 12 27
 prof tsqr_fold_n16 tsqr_fold stage1 16 27
