@@ -33,17 +33,22 @@ struct GramCfg {
   static constexpr int NPAD = 8 * NB;
   static constexpr int NW = 8;  // whole multiples of 4 warps: 6 would leave two SM sub-partitions half idle
   static constexpr int NS = 2;
-  // OP_SOLVE beyond 32 columns: blocked substitution on the tensor cores (8 x 8 diagonal blocks by
-  // their explicit inverses, everything off the diagonal as DMMA updates) instead of lane = row
-  static constexpr bool kBlockedSolve = OP == OP_SOLVE && NB >= 5;
+  // OP_SOLVE: blocked substitution on the tensor cores (8 x 8 diagonal blocks by their explicit
+  // inverses, everything off the diagonal as DMMA updates) instead of lane = row
+#ifndef SQB_BLOCKED_FROM
+#define SQB_BLOCKED_FROM 2  // measured: 4-9 % faster than lane = row substitution already at 16..32 columns
+#endif
+  static constexpr bool kBlockedSolve = OP == OP_SOLVE && NB >= SQB_BLOCKED_FROM;
   // streaming panel heights: P == 8 (mod 16) keeps the plain fragment pattern unpadded, P == 0
   // (mod 16) costs the transposed pattern only 4 pad rows
   static constexpr int kPlainP[8] = {120, 72, 40, 40, 24, 24, 24, 24};
   static constexpr int kMultP[8] = {112, 64, 48, 32, 32, 16, 16, 16};
   // OP_SOLVE: one lane substitutes one row, so the panel height is a multiple of 32
   static constexpr int kSolveP[8] = {64, 64, 32, 32, 16, 16, 16, 16};
+  static constexpr int kBlockedP[8] = {64, 64, 48, 32, 16, 16, 16, 16};  // == 0 (mod 16): pitch P + 4
   static constexpr int P =
-      OP == OP_SOLVE ? kSolveP[NB - 1] : (OP == OP_PLAIN ? kPlainP[NB - 1] : kMultP[NB - 1]);
+      kBlockedSolve ? kBlockedP[NB - 1]
+                    : (OP == OP_SOLVE ? kSolveP[NB - 1] : (OP == OP_PLAIN ? kPlainP[NB - 1] : kMultP[NB - 1]));
   static constexpr int PP = stage_pitch(P, (OP == OP_MULTIPLY || kBlockedSolve) ? 4 : 8);
   static constexpr int kStageDoubles = NPAD * PP;
   static constexpr int kVbuf = 0;
