@@ -169,5 +169,8 @@ if clk.exists():
 tests = G / f"{tag}_gpu_tests.txt"
 if tests.exists():
     out.append(f"\n## GPU tests on the same box\n\n```\n{tests.read_text().strip()}\n```")
+san = G / f"{tag}_sanitizer.txt"
+if san.exists():
+    out.append(f"\n## compute-sanitizer (memcheck on the GPU parity suite, racecheck on the Gram / TSQR parity tests)\n\n```\n{san.read_text().strip()}\n```")
 (P / "README.md").write_text("\n".join(out) + "\n")
 print("wrote", P / "README.md")
