@@ -216,6 +216,7 @@ class Context:
             self.handle = None
             _raise(st, -1, "sqb_create")
         self.device = device
+        self._torch_stream = -1  # cudaStream_t of torch's current stream once device tensors are used
 
     def close(self):
         if getattr(self, "handle", None):
@@ -242,11 +243,13 @@ class Context:
         self._check(self.lib.sqb_set_stream(self.handle, C.c_void_p(cuda_stream_ptr or None)), "set_stream")
 
     def use_own_stream(self):
+        self._torch_stream = -1
         self._check(self.lib.sqb_use_own_stream(self.handle), "use_own_stream")
 
     def use_torch_stream(self):
         import torch
-        self.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
+        self._torch_stream = torch.cuda.current_stream(self.device).cuda_stream
+        self.set_stream(self._torch_stream)
 
     def synchronize(self, where="synchronize"):
         self._check(self.lib.sqb_sync(self.handle), where)
@@ -272,6 +275,12 @@ class Context:
         import torch
         if t.dtype != torch.float64 or not t.is_cuda:
             raise ArgumentError("device inputs must be float64 CUDA tensors")
+        # device tensors are produced by torch kernels on torch's current stream: enqueue behind them
+        # (an own stream would race with the producer of `t`); host-pointer calls keep the own stream
+        cur = torch.cuda.current_stream(self.device).cuda_stream
+        if cur != self._torch_stream:
+            self.set_stream(cur)
+            self._torch_stream = cur
         if t.dim() == 1:
             return C.c_void_p(t.data_ptr()), t.shape[0], 1, max(t.shape[0], 1)
         m, n = t.shape
