@@ -359,6 +359,12 @@ def main():
     if world == 1 and not args.no_sweep:
         del x
         torch.cuda.empty_cache()
+        # the reference's Roofline model (perf_model.hpp) with this box's measured copy bandwidth
+        from paper_2603_20889_b200 import perf_model as pmod
+        hw = pmod.find_hardware("B200")
+        hw.mem_bandwidth = peak * 1e9
+        out["model_hardware"] = {"name": hw.name, "mem_bandwidth": hw.mem_bandwidth, "peak_fp64": hw.peak_fp64,
+                                 "machine_balance": pmod.machine_balance(hw)}
         sweep = []
         for nn in (1, 2, 4, 8, 16, 32, 64):
             xs = ctx.fill_gaussian(m, nn, seed=1234)
@@ -367,7 +373,9 @@ def main():
                 try:
                     ms, _ = timed(lambda: run_method(xs, meth), args.sweep_reps, 2)
                     gbs = 8.0 * m * nn / (ms * 1e-3) / 1e9
-                    row[meth] = {"ms": ms, "gbs": gbs, "frac_8TBs": gbs / NOMINAL_HBM_GBS, "frac_measured": gbs / peak}
+                    model_s = pmod.composite_time(hw, meth, m, nn)
+                    row[meth] = {"ms": ms, "gbs": gbs, "frac_8TBs": gbs / NOMINAL_HBM_GBS, "frac_measured": gbs / peak,
+                                 "model_time_s": model_s, "model_ratio": ms * 1e-3 / model_s}
                     if meth == "tsqr":
                         row[meth]["fp64_tflops_2mn2"] = 2.0 * m * nn * nn / (ms * 1e-3) / 1e12
                 except sq.Error as exc:

@@ -56,13 +56,17 @@ if bench:
         out.append(f"* `bench.py --impl reference`: {ref['value']:.2f} GB/s ({ref['cpu_baseline']['sample']})")
     if "sweep" in bench:
         out.append("\n## Column sweep at m = 2^27 (BASELINE configs[1]); ms / effective GB/s (8mn / t) / % of 8 TB/s\n")
+        if "model_hardware" in bench:
+            out.append(f"Roofline model of the reference (perf_model.hpp, `paper_2603_20889_b200/perf_model.py`) with {bench['model_hardware']}; "
+                       "`x model` = measured time / model time.\n")
         out.append("| n | GiB | TSQR | CholQR2 | SVQB2 | TSQR TFLOP/s (2mn^2) |")
         out.append("|---|---|---|---|---|---|")
         for row in bench["sweep"]:
             cells = []
             for meth in ("tsqr", "cholqr2", "svqb2"):
                 v = row.get(meth, {})
-                cells.append(f"{v['ms']:.2f} ms / {v['gbs']:.0f} / {100*v['frac_8TBs']:.1f} %" if "ms" in v else str(v))
+                cells.append((f"{v['ms']:.2f} ms / {v['gbs']:.0f} / {100*v['frac_8TBs']:.1f} %"
+                              + (f" / {v['model_ratio']:.2f}x model" if "model_ratio" in v else "")) if "ms" in v else str(v))
             out.append(f"| {row['n']} | {row['gib']:.0f} | {cells[0]} | {cells[1]} | {cells[2]} | {row['tsqr'].get('fp64_tflops_2mn2', 0):.1f} |")
 
 # launch list
