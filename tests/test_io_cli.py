@@ -123,3 +123,17 @@ def test_device_stream_and_cli_end_to_end(tmp_path, oracle):
     assert all(r["large_reads"] == (1 if r["method"] == "tsqr" else 2) * r["m"] * r["n"] for r in good)
     assert all(r["orth_resid"] == "ArgumentError" for r in rows if r["n"] == 65)  # per-row error, the grid continues
     assert run_cli("bench", "--reps", "0").returncode != 0
+
+
+def test_cpp_io_header(tmp_path):
+    """The header-only C++ mirror reads the reference-written golden file and writes a byte-identical copy."""
+    import shutil
+    gxx = shutil.which("g++")
+    if gxx is None:
+        pytest.skip("no g++")
+    exe = tmp_path / "io"
+    subprocess.run([gxx, "-std=c++17", "-I", str(ROOT / "paper_2603_20889_b200" / "include"), "-I", str(ROOT / "include"),
+                    str(ROOT / "tests" / "cpp" / "test_io.cpp"), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe), str(GOLDEN), str(tmp_path / "copy.tskm")], capture_output=True, text=True)
+    assert out.returncode == 0 and "ok" in out.stdout
+    assert (tmp_path / "copy.tskm").read_bytes() == GOLDEN.read_bytes()
