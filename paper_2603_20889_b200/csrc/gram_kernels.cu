@@ -46,6 +46,7 @@ struct GramCfg {
   // OP_SOLVE: one lane substitutes one row, so the panel height is a multiple of 32
   static constexpr int kSolveP[8] = {64, 64, 32, 32, 16, 16, 16, 16};
   static constexpr int kBlockedP[8] = {64, 64, 48, 32, 16, 16, 16, 16};  // == 0 (mod 16): pitch P + 4
+  static constexpr int kSolveUnroll = NB <= 2 ? 4 : (NB <= 4 ? 2 : 1);   // row groups solved together
   static constexpr int P =
       kBlockedSolve ? kBlockedP[NB - 1]
                     : (OP == OP_SOLVE ? kSolveP[NB - 1] : (OP == OP_PLAIN ? kPlainP[NB - 1] : kMultP[NB - 1]));
@@ -206,47 +207,67 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
       // written back to the stage, where later blocks read them as B fragments (row g, column 4k+q).
       double* wstage = my + s * Cfg::kStageDoubles;
       const double* dinv = inv + NPAD;
+      // TU row groups advance together: their chains are independent (ILP for the latency-bound narrow
+      // cases) and they share the three warp barriers of a block
+      constexpr int TU = Cfg::kSolveUnroll;
+      static_assert(!Cfg::kBlockedSolve || (P / 8) % TU == 0, "row groups per panel");
 #pragma unroll 1
-      for (int t = 0; t < P / 8; ++t) {
-        double2 y[NB];
+      for (int t0 = 0; t0 < P / 8; t0 += TU) {
+        double2 y[TU][NB];
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
-          double* own = wstage + (8 * b + g) * PP + 8 * t + 2 * q;
-          const double2 x2 = *reinterpret_cast<const double2*>(own);
-          double z0 = x2.x, z1 = x2.y;
+          double* own = wstage + (8 * b + g) * PP + 8 * t0 + 2 * q;
+          double z[TU][2];
+#pragma unroll
+          for (int u = 0; u < TU; ++u) {
+            const double2 x2 = *reinterpret_cast<const double2*>(own + 8 * u);
+            z[u][0] = x2.x;
+            z[u][1] = x2.y;
+          }
 #pragma unroll
           for (int a = 0; a < b; ++a) {
 #pragma unroll
             for (int kk = 0; kk < 2; ++kk) {
               const double af = fac[(8 * a + 4 * kk + q) + (8 * b + g) * FP];  // -R_ab
-              const double bf = wstage[(8 * a + 4 * kk + q) * PP + 8 * t + g];
-              dmma884(z0, z1, af, bf);
+#pragma unroll
+              for (int u = 0; u < TU; ++u)
+                dmma884(z[u][0], z[u][1], af, wstage[(8 * a + 4 * kk + q) * PP + 8 * (t0 + u) + g]);
             }
           }
-          *reinterpret_cast<double2*>(own) = make_double2(z0, z1);
+#pragma unroll
+          for (int u = 0; u < TU; ++u) *reinterpret_cast<double2*>(own + 8 * u) = make_double2(z[u][0], z[u][1]);
           __syncwarp();
-          double w0 = 0.0, w1 = 0.0;
+          double w[TU][2];
+#pragma unroll
+          for (int u = 0; u < TU; ++u) w[u][0] = w[u][1] = 0.0;
 #pragma unroll
           for (int kk = 0; kk < 2; ++kk) {
             const double af = dinv[b * 8 * Cfg::kDinvPitch + (4 * kk + q) + Cfg::kDinvPitch * g];
-            const double bf = wstage[(8 * b + 4 * kk + q) * PP + 8 * t + g];
-            dmma884(w0, w1, af, bf);
+#pragma unroll
+            for (int u = 0; u < TU; ++u)
+              dmma884(w[u][0], w[u][1], af, wstage[(8 * b + 4 * kk + q) * PP + 8 * (t0 + u) + g]);
           }
           __syncwarp();  // every lane has read Z_b before Y_b replaces it
-          *reinterpret_cast<double2*>(own) = make_double2(w0, w1);
+#pragma unroll
+          for (int u = 0; u < TU; ++u) {
+            *reinterpret_cast<double2*>(own + 8 * u) = make_double2(w[u][0], w[u][1]);
+            y[u][b] = make_double2(w[u][0], w[u][1]);
+          }
           __syncwarp();
-          y[b] = make_double2(w0, w1);
         }
-        int p = 0;
 #pragma unroll
-        for (int b = 0; b < NB; ++b)
+        for (int u = 0; u < TU; ++u) {
+          int p = 0;
 #pragma unroll
-          for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], y[b].x, y[b2].x);
-        p = 0;
+          for (int b = 0; b < NB; ++b)
 #pragma unroll
-        for (int b = 0; b < NB; ++b)
+            for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], y[u][b].x, y[u][b2].x);
+          p = 0;
 #pragma unroll
-          for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], y[b].y, y[b2].y);
+          for (int b = 0; b < NB; ++b)
+#pragma unroll
+            for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], y[u][b].y, y[u][b2].y);
+        }
       }
       __syncwarp();
       if (pnl + static_cast<long long>(NS) * NW < npanels) issue(pnl + static_cast<long long>(NS) * NW, s);
