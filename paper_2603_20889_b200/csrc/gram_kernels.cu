@@ -46,7 +46,8 @@ struct GramCfg {
   // OP_SOLVE: one lane substitutes one row, so the panel height is a multiple of 32
   static constexpr int kSolveP[8] = {64, 64, 32, 32, 16, 16, 16, 16};
   static constexpr int kBlockedP[8] = {64, 64, 48, 32, 16, 16, 16, 16};  // == 0 (mod 16): pitch P + 4
-  static constexpr int kSolveUnroll = NB <= 2 ? 4 : (NB <= 4 ? 2 : 1);   // row groups solved together
+  static constexpr int kMultUnroll = NB == 1 ? 2 : (NB == 2 ? 4 : (NB == 3 ? 3 : 1));  // measured: no gain from 32 columns on
+  static constexpr int kSolveUnroll = NB <= 2 ? 4 : (NB == 3 ? 3 : (NB == 4 ? 4 : (NB <= 6 ? 2 : 1)));  // row groups solved together
   static constexpr int P =
       kBlockedSolve ? kBlockedP[NB - 1]
                     : (OP == OP_SOLVE ? kSolveP[NB - 1] : (OP == OP_PLAIN ? kPlainP[NB - 1] : kMultP[NB - 1]));
@@ -330,28 +331,42 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
       if (pnl + static_cast<long long>(NS) * NW < npanels) issue(pnl + static_cast<long long>(NS) * NW, s);
     } else {  // OP_MULTIPLY
       const int kchunks = (n + 3) / 4;
-      for (int t = 0; t < P / 8; ++t) {
-        double y[NB][2];
+      // MU row groups advance together: NB * MU independent DMMA chains of length kchunks, and every
+      // factor fragment is loaded once per MU groups
+      constexpr int MU = Cfg::kMultUnroll;
+      static_assert(OP != OP_MULTIPLY || (P / 8) % MU == 0, "row groups per panel");
+#pragma unroll 1
+      for (int t0 = 0; t0 < P / 8; t0 += MU) {
+        double y[MU][NB][2];
 #pragma unroll
-        for (int b = 0; b < NB; ++b) y[b][0] = y[b][1] = 0.0;
+        for (int u = 0; u < MU; ++u)
+#pragma unroll
+          for (int b = 0; b < NB; ++b) y[u][b][0] = y[u][b][1] = 0.0;
+#pragma unroll 1
         for (int kc = 0; kc < kchunks; ++kc) {
-          const double bf = stage[(4 * kc + q) * PP + 8 * t + g];
+          double bf[MU];
+#pragma unroll
+          for (int u = 0; u < MU; ++u) bf[u] = stage[(4 * kc + q) * PP + 8 * (t0 + u) + g];
 #pragma unroll
           for (int b = 0; b < NB; ++b) {
             const double af = fac[(4 * kc + q) + (8 * b + g) * FP];
-            dmma884(y[b][0], y[b][1], af, bf);
+#pragma unroll
+            for (int u = 0; u < MU; ++u) dmma884(y[u][b][0], y[u][b][1], af, bf[u]);
           }
         }
-        int p = 0;
 #pragma unroll
-        for (int b = 0; b < NB; ++b)
+        for (int u = 0; u < MU; ++u) {
+          int p = 0;
 #pragma unroll
-          for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], y[b][0], y[b2][0]);
-        p = 0;
+          for (int b = 0; b < NB; ++b)
 #pragma unroll
-        for (int b = 0; b < NB; ++b)
+            for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], y[u][b][0], y[u][b2][0]);
+          p = 0;
 #pragma unroll
-          for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], y[b][1], y[b2][1]);
+          for (int b = 0; b < NB; ++b)
+#pragma unroll
+            for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], y[u][b][1], y[u][b2][1]);
+        }
       }
       __syncwarp();
       if (pnl + static_cast<long long>(NS) * NW < npanels) issue(pnl + static_cast<long long>(NS) * NW, s);
