@@ -41,7 +41,12 @@ struct GramCfg {
   static constexpr bool kBlockedSolve = OP == OP_SOLVE && NB >= SQB_BLOCKED_FROM;
   // streaming panel heights: P == 8 (mod 16) keeps the plain fragment pattern unpadded, P == 0
   // (mod 16) costs the transposed pattern only 4 pad rows
-  static constexpr int kPlainP[8] = {120, 72, 40, 40, 24, 24, 24, 24};
+#ifndef SQB_GRAM_2CTA
+#define SQB_GRAM_2CTA 0
+#endif
+  // plain Gram at 17..32 columns: two CTAs per SM (shorter panels, half the shared memory, 16 warps)
+  static constexpr int kCtas = (SQB_GRAM_2CTA && OP == OP_PLAIN && (NB == 3 || NB == 4)) ? 2 : 1;
+  static constexpr int kPlainP[8] = {120, 72, kCtas == 2 ? 24 : 40, kCtas == 2 ? 24 : 40, 24, 24, 24, 24};
   static constexpr int kMultP[8] = {112, 64, 48, 32, 32, 16, 16, 16};
   // OP_SOLVE: one lane substitutes one row, so the panel height is a multiple of 32
   static constexpr int kSolveP[8] = {64, 64, 32, 32, 16, 16, 16, 16};
@@ -54,7 +59,7 @@ struct GramCfg {
   static constexpr int PP = stage_pitch(P, (OP == OP_MULTIPLY || kBlockedSolve) ? 4 : 8);
   static constexpr int kStageDoubles = NPAD * PP;
   static constexpr int kVbuf = 0;
-  static constexpr int kWarpDoubles = NS * kStageDoubles + kVbuf + 2 * NS;  // + mbarrier slots
+  static constexpr int kWarpDoubles = NS * kStageDoubles + kVbuf;
   static constexpr int FP = NPAD + 4;  // factor pitch: conflict-free A-fragment reads
   static constexpr int kDinvPitch = 12;  // (4k+q) + 12 g: conflict-free A-fragment reads of an 8 x 8 block
   static constexpr int kFacDoubles =
@@ -69,7 +74,7 @@ struct GramCfg {
 };
 
 template <int NB, int OP>
-__global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
+__global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, GramCfg<NB, OP>::kCtas)
     gram_mma_kernel(const GramParams prm) {
   using Cfg = GramCfg<NB, OP>;
   constexpr int P = Cfg::P, PP = Cfg::PP, NW = Cfg::NW, NS = Cfg::NS, NPAD = Cfg::NPAD;
@@ -82,7 +87,12 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, 1)
 
   double* my = smem + static_cast<size_t>(warp) * Cfg::kWarpDoubles;
   double* vbuf = my + NS * Cfg::kStageDoubles;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(vbuf + Cfg::kVbuf);
+  // the mbarriers live OUTSIDE the dynamic stage area: that area is repurposed as the CTA sum at the
+  // end, and the memory of a live mbarrier object must not be overwritten (PTX: mbarrier.inval first);
+  // racecheck runs of the aliased layout produced intermittent NaNs from 40 columns on
+  __shared__ uint64_t bars_all[NW * NS];
+  uint64_t* bars = bars_all + warp * NS;
+  (void)vbuf;
   double* fac = smem + static_cast<size_t>(NW) * Cfg::kWarpDoubles;  // NPAD x FP, then inv diag
   double* inv = fac + NPAD * FP;
   double* csum = smem;  // reused once every warp has left the streaming loop
@@ -481,6 +491,10 @@ int gram_warps(int n) {
   return 8;
 }
 
-int gram_ctas_per_sm(int n, int op) { return n <= kThreadGramMaxN ? gram_thread_ctas_per_sm(n, op) : 1; }
+int gram_ctas_per_sm(int n, int op) {
+  if (n <= kThreadGramMaxN) return gram_thread_ctas_per_sm(n, op);
+  const int nb = (n + 7) / 8;
+  return (SQB_GRAM_2CTA && op == OP_PLAIN && (nb == 3 || nb == 4)) ? 2 : 1;
+}
 
 }  // namespace sqb

@@ -33,6 +33,5 @@ prof gram_mma_n64 gram_mma tsmttsm 64 25
 prof gram_wide_n128 gram_wide_kernel tsmttsm 128 23
 prof gram_wide_n256 gram_wide_kernel tsmttsm 256 22
 python tools/run_configs.py $TAG > $O/${TAG}_configs.log 2>&1
-compute-sanitizer --tool memcheck python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "not kernel_family and not dropin" 2>&1 | tail -4 > $O/${TAG}_sanitizer.txt
-compute-sanitizer --tool racecheck python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "wide_gram or test_gram_kernels or test_tsqr_parity" 2>&1 | tail -3 >> $O/${TAG}_sanitizer.txt
+bash tools/sanitize.sh > /dev/null 2>&1
 ls -la $O
