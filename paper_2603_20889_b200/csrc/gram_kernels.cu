@@ -42,17 +42,24 @@ struct GramCfg {
   // streaming panel heights: P == 8 (mod 16) keeps the plain fragment pattern unpadded, P == 0
   // (mod 16) costs the transposed pattern only 4 pad rows
 #ifndef SQB_GRAM_2CTA
-#define SQB_GRAM_2CTA 0
+#define SQB_GRAM_2CTA 1
 #endif
   // plain Gram at 17..32 columns: two CTAs per SM (shorter panels, half the shared memory, 16 warps)
-  static constexpr int kCtas = (SQB_GRAM_2CTA && OP == OP_PLAIN && (NB == 3 || NB == 4)) ? 2 : 1;
+#ifndef SQB_GRAM_2CTA_ALL
+#define SQB_GRAM_2CTA_ALL 1
+#endif
+#ifndef SQB_GRAM_2CTA_NB2
+#define SQB_GRAM_2CTA_NB2 1
+#endif
+  static constexpr int kCtas = ((SQB_GRAM_2CTA && (OP == OP_PLAIN || SQB_GRAM_2CTA_ALL) && (NB == 3 || NB == 4)) ||
+                                (SQB_GRAM_2CTA_NB2 && OP != OP_PLAIN && NB == 2)) ? 2 : 1;
   static constexpr int kPlainP[8] = {120, 72, kCtas == 2 ? 24 : 40, kCtas == 2 ? 24 : 40, 24, 24, 24, 24};
-  static constexpr int kMultP[8] = {112, 64, 48, 32, 32, 16, 16, 16};
+  static constexpr int kMultP[8] = {112, kCtas == 2 ? 32 : 64, kCtas == 2 ? 16 : 48, kCtas == 2 ? 16 : 32, 32, 16, 16, 16};
   // OP_SOLVE: one lane substitutes one row, so the panel height is a multiple of 32
   static constexpr int kSolveP[8] = {64, 64, 32, 32, 16, 16, 16, 16};
-  static constexpr int kBlockedP[8] = {64, 64, 48, 32, 16, 16, 16, 16};  // == 0 (mod 16): pitch P + 4
-  static constexpr int kMultUnroll = NB == 1 ? 2 : (NB == 2 ? 4 : (NB == 3 ? 3 : 1));  // measured: no gain from 32 columns on
-  static constexpr int kSolveUnroll = NB <= 2 ? 4 : (NB == 3 ? 3 : (NB == 4 ? 4 : (NB <= 6 ? 2 : 1)));  // row groups solved together
+  static constexpr int kBlockedP[8] = {64, kCtas == 2 ? 32 : 64, kCtas == 2 ? 16 : 48, kCtas == 2 ? 16 : 32, 16, 16, 16, 16};  // == 0 (mod 16): pitch P + 4
+  static constexpr int kMultUnroll = NB == 1 ? 2 : (NB == 2 ? 4 : (NB == 3 ? (kCtas == 2 ? 2 : 3) : 1));  // measured: no gain from 32 columns on
+  static constexpr int kSolveUnroll = NB <= 2 ? 4 : (kCtas == 2 ? 2 : (NB == 3 ? 3 : (NB == 4 ? 4 : (NB <= 6 ? 2 : 1))));  // row groups solved together
   static constexpr int P =
       kBlockedSolve ? kBlockedP[NB - 1]
                     : (OP == OP_SOLVE ? kSolveP[NB - 1] : (OP == OP_PLAIN ? kPlainP[NB - 1] : kMultP[NB - 1]));
@@ -494,7 +501,8 @@ int gram_warps(int n) {
 int gram_ctas_per_sm(int n, int op) {
   if (n <= kThreadGramMaxN) return gram_thread_ctas_per_sm(n, op);
   const int nb = (n + 7) / 8;
-  return (SQB_GRAM_2CTA && op == OP_PLAIN && (nb == 3 || nb == 4)) ? 2 : 1;
+  if (SQB_GRAM_2CTA_NB2 && op != OP_PLAIN && nb == 2) return 2;
+  return (SQB_GRAM_2CTA && (op == OP_PLAIN || SQB_GRAM_2CTA_ALL) && (nb == 3 || nb == 4)) ? 2 : 1;
 }
 
 }  // namespace sqb
