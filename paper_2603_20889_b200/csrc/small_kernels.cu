@@ -17,6 +17,10 @@ namespace sqb {
 namespace {
 
 constexpr int kSmallThreads = 256;
+// The Jacobi kernels scale their thread count with n: a round of the 64 x 64 problem rotates 2 x 2048
+// column / row entries of A and U, which 256 threads walk in 8 trips between CTA barriers.
+constexpr int kJacobiMaxThreads = 1024;
+inline int jacobi_threads(int n) { return n <= 16 ? 256 : (n <= 40 ? 512 : 1024); }
 constexpr double kEps = 2.220446049250313e-16;  // std::numeric_limits<double>::epsilon()
 
 // ------------------------------------------------------------------------------------------------
@@ -89,16 +93,16 @@ struct JacobiScratch {
   double* dqq;   // np/2
   int* pp;       // np/2
   int* qq;       // np/2
-  double* red;   // kSmallThreads
+  double* red;   // kJacobiMaxThreads
   int* perm;     // n
 };
 
 __device__ double block_sum(double v, double* red) {
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, nt_ = blockDim.x;
   __syncthreads();
   red[tid] = v;
   __syncthreads();
-  for (int s = kSmallThreads / 2; s > 0; s >>= 1) {
+  for (int s = nt_ / 2; s > 0; s >>= 1) {
     if (tid < s) red[tid] += red[tid + s];
     __syncthreads();
   }
@@ -108,19 +112,19 @@ __device__ double block_sum(double v, double* red) {
 }
 
 __device__ bool jacobi_eigh(double* a, int lda, double* u, int ldu, int n, const JacobiScratch& js) {
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, nt_ = blockDim.x;
   const int np = (n + 1) & ~1;
   const int half = np / 2;
   // |C|_F and identity U
   double fro = 0.0;
-  for (int idx = tid; idx < n * n; idx += kSmallThreads) {
+  for (int idx = tid; idx < n * n; idx += nt_) {
     const int i = idx % n, j = idx / n;
     const double v = a[i + j * lda];
     fro = fma(v, v, fro);
     u[i + j * ldu] = i == j ? 1.0 : 0.0;
   }
   if (np > n) {  // padding index: zero row/column, never rotated (a_pq == 0 rule)
-    for (int i = tid; i < np; i += kSmallThreads) {
+    for (int i = tid; i < np; i += nt_) {
       a[i + n * lda] = 0.0;
       a[n + i * lda] = 0.0;
     }
@@ -129,7 +133,7 @@ __device__ bool jacobi_eigh(double* a, int lda, double* u, int ldu, int n, const
 
   auto offdiag = [&]() {
     double s = 0.0;
-    for (int idx = tid; idx < n * n; idx += kSmallThreads) {
+    for (int idx = tid; idx < n * n; idx += nt_) {
       const int i = idx % n, j = idx / n;
       if (i < j) s = fma(a[i + j * lda], a[i + j * lda], s);
     }
@@ -172,7 +176,7 @@ __device__ bool jacobi_eigh(double* a, int lda, double* u, int ldu, int n, const
       }
       __syncthreads();
       // phase B: columns  A <- A J,  U <- U J
-      for (int idx = tid; idx < half * np; idx += kSmallThreads) {
+      for (int idx = tid; idx < half * np; idx += nt_) {
         const int t = idx / np, i = idx % np;
         const int p = js.pp[t];
         if (p < 0) continue;
@@ -189,7 +193,7 @@ __device__ bool jacobi_eigh(double* a, int lda, double* u, int ldu, int n, const
       }
       __syncthreads();
       // phase C: rows  A <- J^T A
-      for (int idx = tid; idx < half * np; idx += kSmallThreads) {
+      for (int idx = tid; idx < half * np; idx += nt_) {
         const int t = idx / np, j = idx % np;
         const int p = js.pp[t];
         if (p < 0) continue;
@@ -213,9 +217,9 @@ __device__ bool jacobi_eigh(double* a, int lda, double* u, int ldu, int n, const
     converged = offdiag() <= thr;
   }
   // stable descending rank (gram_qr.cpp:107-110)
-  for (int j = tid; j < n; j += kSmallThreads) js.perm[j] = j;
+  for (int j = tid; j < n; j += nt_) js.perm[j] = j;
   __syncthreads();
-  for (int j = tid; j < n; j += kSmallThreads) {
+  for (int j = tid; j < n; j += nt_) {
     const double lj = a[j + j * lda];
     int rank = 0;
     for (int i = 0; i < n; ++i) {
@@ -246,7 +250,7 @@ __host__ __device__ inline SmallLayout small_layout(int n) {
   if (L.u_in_smem) off += static_cast<size_t>(n) * L.ldu;
   L.misc_off = off;
   // cs, sn, dpp, dqq (np/2 each), pp, qq (np/2 ints each -> np/2 doubles), red, perm (n ints)
-  off += 4 * (np / 2) + (np / 2) + kSmallThreads + (n + 1) / 2 + 4;
+  off += 4 * (np / 2) + (np / 2) + kJacobiMaxThreads + (n + 1) / 2 + 4;
   L.total_doubles = off;
   return L;
 }
@@ -262,12 +266,12 @@ __device__ JacobiScratch carve_scratch(double* sm, const SmallLayout& L, int n) 
   js.pp = reinterpret_cast<int*>(p);
   js.qq = js.pp + np / 2;
   p += np / 2;
-  js.red = p; p += kSmallThreads;
+  js.red = p; p += kJacobiMaxThreads;
   js.perm = reinterpret_cast<int*>(p);
   return js;
 }
 
-__global__ void __launch_bounds__(kSmallThreads)
+__global__ void __launch_bounds__(kJacobiMaxThreads)
     eigh_kernel(const double* __restrict__ c, int n, double* values, double* vectors,
                 double* gscratch, StatusWord* status) {
   extern __shared__ __align__(16) double sm[];
@@ -275,13 +279,13 @@ __global__ void __launch_bounds__(kSmallThreads)
   double* a = sm + L.a_off;
   double* u = L.u_in_smem ? sm + L.u_off : gscratch;
   const JacobiScratch js = carve_scratch(sm, L, n);
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < n * n; idx += kSmallThreads) a[idx % n + (idx / n) * L.lda] = c[idx];
+  const int tid = threadIdx.x, nt_ = blockDim.x;
+  for (int idx = tid; idx < n * n; idx += nt_) a[idx % n + (idx / n) * L.lda] = c[idx];
   __syncthreads();
   const bool ok = jacobi_eigh(a, L.lda, u, L.ldu, n, js);
   if (!ok && tid == 0) raise_status(status, SQB_E_NO_CONVERGENCE, -1);
-  for (int j = tid; j < n; j += kSmallThreads) values[j] = a[js.perm[j] + js.perm[j] * L.lda];
-  for (int idx = tid; idx < n * n; idx += kSmallThreads) {
+  for (int j = tid; j < n; j += nt_) values[j] = a[js.perm[j] + js.perm[j] * L.lda];
+  for (int idx = tid; idx < n * n; idx += nt_) {
     const int i = idx % n, j = idx / n;
     vectors[idx] = u[i + js.perm[j] * L.ldu];
   }
@@ -291,7 +295,7 @@ __global__ void __launch_bounds__(kSmallThreads)
 // eigen-decomposition of D C D, rank = #{lambda >= 10 n eps lambda_max}, B = D U L^-1/2,
 // Z = L^1/2 U^T D^-1 with truncated columns/rows exactly zero; sigma = sqrt(max(eig(C), 0)) from a
 // second eigen-decomposition of the unscaled Gram matrix.
-__global__ void __launch_bounds__(kSmallThreads)
+__global__ void __launch_bounds__(kJacobiMaxThreads)
     svqb_pass_kernel(const double* __restrict__ c, int n, double* bmat, double* z, double* sigma,
                      long long* rank_out, int want_sigma, double* gscratch, StatusWord* status) {
   extern __shared__ __align__(16) double sm[];
@@ -303,16 +307,16 @@ __global__ void __launch_bounds__(kSmallThreads)
   const JacobiScratch js = carve_scratch(sm, L, n);
   __shared__ int rank_s;
   __shared__ int fail_s;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, nt_ = blockDim.x;
 
-  for (int j = tid; j < n; j += kSmallThreads) {
+  for (int j = tid; j < n; j += nt_) {
     const double d = c[j + j * n];
     ds[j] = d > 0.0 ? 1.0 / sqrt(d) : 1.0;
     dsi[j] = d > 0.0 ? sqrt(d) : 1.0;
   }
   if (tid == 0) fail_s = 0;
   __syncthreads();
-  for (int idx = tid; idx < n * n; idx += kSmallThreads) {
+  for (int idx = tid; idx < n * n; idx += nt_) {
     const int i = idx % n, j = idx / n;
     a[i + j * L.lda] = c[idx] * ds[i] * ds[j];
   }
@@ -342,7 +346,7 @@ __global__ void __launch_bounds__(kSmallThreads)
   }
   __syncthreads();
   const int rank = rank_s;
-  for (int idx = tid; idx < n * n; idx += kSmallThreads) {
+  for (int idx = tid; idx < n * n; idx += nt_) {
     const int i = idx % n, j = idx / n;
     double bv = 0.0, zv = 0.0;
     if (j < rank && !fail_s) {
@@ -357,11 +361,11 @@ __global__ void __launch_bounds__(kSmallThreads)
   }
   __syncthreads();
   if (want_sigma) {
-    for (int idx = tid; idx < n * n; idx += kSmallThreads) a[idx % n + (idx / n) * L.lda] = c[idx];
+    for (int idx = tid; idx < n * n; idx += nt_) a[idx % n + (idx / n) * L.lda] = c[idx];
     __syncthreads();
     ok = jacobi_eigh(a, L.lda, u, L.ldu, n, js);
     if (!ok && tid == 0) raise_status(status, SQB_E_NO_CONVERGENCE, -1);
-    for (int j = tid; j < n; j += kSmallThreads)
+    for (int j = tid; j < n; j += nt_)
       sigma[j] = sqrt(fmax(a[js.perm[j] + js.perm[j] * L.lda], 0.0));
   }
 }
@@ -492,7 +496,7 @@ cudaError_t launch_eigh(const double* c, int n, double* values, double* vectors,
   const size_t bytes = small_smem_bytes(n);
   cudaError_t e = opt_in_smem(eigh_kernel, bytes);
   if (e != cudaSuccess) return e;
-  eigh_kernel<<<1, kSmallThreads, bytes, stream>>>(c, n, values, vectors, scratch, status);
+  eigh_kernel<<<1, jacobi_threads(n), bytes, stream>>>(c, n, values, vectors, scratch, status);
   return cudaGetLastError();
 }
 
@@ -502,7 +506,7 @@ cudaError_t launch_svqb_pass(const double* c, int n, double* b, double* z, doubl
   const size_t bytes = small_smem_bytes(n);
   cudaError_t e = opt_in_smem(svqb_pass_kernel, bytes);
   if (e != cudaSuccess) return e;
-  svqb_pass_kernel<<<1, kSmallThreads, bytes, stream>>>(c, n, b, z, sigma, rank, want_sigma, scratch,
+  svqb_pass_kernel<<<1, jacobi_threads(n), bytes, stream>>>(c, n, b, z, sigma, rank, want_sigma, scratch,
                                                         status);
   return cudaGetLastError();
 }
