@@ -20,7 +20,11 @@ constexpr int kSmallThreads = 256;
 // The Jacobi kernels scale their thread count with n: a round of the 64 x 64 problem rotates 2 x 2048
 // column / row entries of A and U, which 256 threads walk in 8 trips between CTA barriers.
 constexpr int kJacobiMaxThreads = 1024;
-inline int jacobi_threads(int n) { return n <= 16 ? 256 : (n <= 40 ? 512 : 1024); }
+// one warp per rotation pair of a round (n/2 pairs), at most 32 warps
+inline int jacobi_threads(int n) {
+  const int warps = (n + 1) / 2;
+  return warps <= 8 ? 256 : (warps <= 16 ? 512 : (warps <= 24 ? 768 : 1024));
+}
 constexpr double kEps = 2.220446049250313e-16;  // std::numeric_limits<double>::epsilon()
 
 // ------------------------------------------------------------------------------------------------
@@ -82,10 +86,31 @@ __global__ void __launch_bounds__(kSmallThreads)
 // stopping test off(A) <= 10*n*eps*|C|_F checked once per sweep, 30-sweep cap and stable
 // descending sort (gram_qr.cpp:60-121).  The reference sweeps cyclic-by-row, one rotation at a
 // time; here the n/2 disjoint rotations of a round-robin round are applied together (column
-// phase, row phase), which is what lets one CTA finish a 64 x 64 problem in ~0.1 ms.
+// phase, row phase; one warp per pair, two CTA barriers per round).
 // `a` (np x lda, np = n rounded up to even) and `u` (n x ldu) are CTA-visible scratch.
 // Returns false when the sweep cap is hit.  On return perm[j] = source column of output j.
 // ------------------------------------------------------------------------------------------------
+// The rotation scalars are a serial chain of two divisions, a square root and a reciprocal square root
+// per round; the IEEE software sequences for those cost ~3000 clk per round, i.e. most of the solver.
+// MUFU seed + two Newton steps each (<= 1-2 ulp) take a tenth of that; the eigen-decomposition is
+// compared through its invariants, never bitwise.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double z;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(z) : "d"(x));
+  double e = fma(-x, z, 1.0);
+  z = fma(z, e, z);
+  e = fma(-x, z, 1.0);
+  return fma(z, e, z);
+}
+__device__ __forceinline__ double fast_rsqrt(double x) {  // x in [1, 1e200]
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+
 struct JacobiScratch {
   double* cs;    // np/2
   double* sn;    // np/2
@@ -143,74 +168,85 @@ __device__ bool jacobi_eigh(double* a, int lda, double* u, int ldu, int n, const
   bool converged = offdiag() <= thr;
   for (int sweep = 0; sweep < 30 && !converged; ++sweep) {
     for (int step = 0; step < np - 1; ++step) {
-      // phase A: rotation parameters of this round's pairs
-      if (tid < half) {
+      // A WARP owns a pair of the round: every lane derives the rotation itself (no parameter
+      // exchange, no barrier between "parameters" and "columns"), then the lanes share the rows.
+      // Pairs of one round are disjoint, and the entries a_pp, a_qq, a_pq a warp reads here are only
+      // ever written by that warp (columns) or after the CTA barrier (rows).
+      const int warp = tid >> 5, lane = tid & 31, nwarps = nt_ >> 5;
+      for (int t = warp; t < half; t += nwarps) {
         int x, y;
-        if (tid == 0) {
+        if (t == 0) {
           x = np - 1;
           y = step;
         } else {
-          x = (step + tid) % (np - 1);
-          y = (step - tid + (np - 1)) % (np - 1);
+          x = (step + t) % (np - 1);
+          y = (step - t + (np - 1)) % (np - 1);
         }
         const int p = min(x, y), q = max(x, y);
         const double apq = a[p + q * lda];
         double cs = 1.0, sn = 0.0, npp = 0.0, nqq = 0.0;
-        int pmark = -1;
-        if (apq != 0.0) {
+        const bool rot = apq != 0.0;
+        if (rot) {
           const double app = a[p + p * lda], aqq = a[q + q * lda];
-          const double theta = (aqq - app) / (2.0 * apq);
-          const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
-          cs = 1.0 / sqrt(1.0 + t * t);
-          sn = t * cs;
-          npp = app - t * apq;
-          nqq = aqq + t * apq;
-          pmark = p;
+          const double theta = (aqq - app) * fast_rcp(2.0 * apq);
+          const double ath = fabs(theta);
+          double tt;
+          if (ath < 1e100) {
+            const double r2 = fma(theta, theta, 1.0);
+            const double y = fast_rsqrt(r2);
+            double sq = r2 * y;
+            sq = fma(fma(-sq, sq, r2), 0.5 * y, sq);  // sqrt(1 + theta^2), residual-corrected
+            tt = (theta >= 0.0 ? 1.0 : -1.0) * fast_rcp(ath + sq);
+          } else {
+            tt = 0.5 / theta;  // sqrt(1 + theta^2) == |theta| in working precision (also theta = +-inf)
+          }
+          cs = fast_rsqrt(fma(tt, tt, 1.0));
+          sn = tt * cs;
+          npp = app - tt * apq;
+          nqq = aqq + tt * apq;
         }
-        js.cs[tid] = cs;
-        js.sn[tid] = sn;
-        js.dpp[tid] = npp;
-        js.dqq[tid] = nqq;
-        js.pp[tid] = pmark;
-        js.qq[tid] = q;
+        if (lane == 0) {
+          js.cs[t] = cs;
+          js.sn[t] = sn;
+          js.dpp[t] = npp;
+          js.dqq[t] = nqq;
+          js.pp[t] = rot ? p : -1;
+          js.qq[t] = q;
+        }
+        __syncwarp();  // every lane has read a_pp, a_qq, a_pq before the columns change
+        if (rot) {
+          // columns  A <- A J,  U <- U J
+          for (int i = lane; i < np; i += 32) {
+            const double aip = a[i + p * lda], aiq = a[i + q * lda];
+            a[i + p * lda] = cs * aip - sn * aiq;
+            a[i + q * lda] = sn * aip + cs * aiq;
+            if (i < n) {
+              const double uip = u[i + p * ldu], uiq = u[i + q * ldu];
+              u[i + p * ldu] = cs * uip - sn * uiq;
+              u[i + q * ldu] = sn * uip + cs * uiq;
+            }
+          }
+        }
       }
       __syncthreads();
-      // phase B: columns  A <- A J,  U <- U J
-      for (int idx = tid; idx < half * np; idx += nt_) {
-        const int t = idx / np, i = idx % np;
+      // rows  A <- J^T A, then the exact 2x2 results (gram_qr.cpp:84-87)
+      for (int t = warp; t < half; t += nwarps) {
         const int p = js.pp[t];
         if (p < 0) continue;
         const int q = js.qq[t];
         const double cs = js.cs[t], sn = js.sn[t];
-        const double aip = a[i + p * lda], aiq = a[i + q * lda];
-        a[i + p * lda] = cs * aip - sn * aiq;
-        a[i + q * lda] = sn * aip + cs * aiq;
-        if (i < n) {
-          const double uip = u[i + p * ldu], uiq = u[i + q * ldu];
-          u[i + p * ldu] = cs * uip - sn * uiq;
-          u[i + q * ldu] = sn * uip + cs * uiq;
+        for (int j = lane; j < np; j += 32) {
+          const double apj = a[p + j * lda], aqj = a[q + j * lda];
+          a[p + j * lda] = cs * apj - sn * aqj;
+          a[q + j * lda] = sn * apj + cs * aqj;
         }
-      }
-      __syncthreads();
-      // phase C: rows  A <- J^T A
-      for (int idx = tid; idx < half * np; idx += nt_) {
-        const int t = idx / np, j = idx % np;
-        const int p = js.pp[t];
-        if (p < 0) continue;
-        const int q = js.qq[t];
-        const double cs = js.cs[t], sn = js.sn[t];
-        const double apj = a[p + j * lda], aqj = a[q + j * lda];
-        a[p + j * lda] = cs * apj - sn * aqj;
-        a[q + j * lda] = sn * apj + cs * aqj;
-      }
-      __syncthreads();
-      // phase D: exact 2x2 results (gram_qr.cpp:84-87)
-      if (tid < half && js.pp[tid] >= 0) {
-        const int p = js.pp[tid], q = js.qq[tid];
-        a[p + p * lda] = js.dpp[tid];
-        a[q + q * lda] = js.dqq[tid];
-        a[p + q * lda] = 0.0;
-        a[q + p * lda] = 0.0;
+        __syncwarp();
+        if (lane == 0) {
+          a[p + p * lda] = js.dpp[t];
+          a[q + q * lda] = js.dqq[t];
+          a[p + q * lda] = 0.0;
+          a[q + p * lda] = 0.0;
+        }
       }
       __syncthreads();
     }
