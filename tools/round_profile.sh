@@ -30,6 +30,15 @@ prof gram_thread_n8 gram_thread tsmttsm 8 27
 prof gram_mma_n16 gram_mma tsmttsm 16 27
 prof gram_mma_n32 gram_mma tsmttsm 32 26
 prof gram_mma_n64 gram_mma tsmttsm 64 25
+prof2() { # the SECOND matching launch of a cholqr2 call = the fused solve + Gram sweep (gram_*_kernel<.., OP_SOLVE>)
+  ncu --set full --clock-control none -k regex:$2 -s 1 -c 1 -o $O/${TAG}_$1 python tools/prof_run.py cholqr2 $3 $4 1 > /dev/null 2>&1
+  ncu -i $O/${TAG}_$1.ncu-rep --page raw --csv > $O/${TAG}_$1.raw.csv 2>/dev/null
+  rm -f $O/${TAG}_$1.ncu-rep
+}
+prof2 gram_solve_n8 gram_thread 8 27
+prof2 gram_solve_n16 gram_mma 16 27
+prof2 gram_solve_n32 gram_mma 32 26
+prof2 gram_solve_n64 gram_mma 64 25
 prof gram_wide_n128 gram_wide_kernel tsmttsm 128 23
 prof gram_wide_n256 gram_wide_kernel tsmttsm 256 22
 python tools/run_configs.py $TAG > $O/${TAG}_configs.log 2>&1
