@@ -44,11 +44,15 @@ __global__ void __launch_bounds__(kSmallThreads)
     const int i = idx % n, j = idx / n;
     a[i + j * ld] = c[idx];
   }
-  if (tid == 0) {
+  __syncthreads();
+  if (tid < 32) {  // max |c_jj| from the shared copy (a serial walk over global memory costs ~0.5 us per entry)
     double mx = 0.0;
-    for (int j = 0; j < n; ++j) mx = fmax(mx, fabs(c[j + j * n]));
-    tol_s = static_cast<double>(n) * kEps * mx;
-    fail_s = -1;
+    for (int j = tid; j < n; j += 32) mx = fmax(mx, fabs(a[j + j * ld]));
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (tid == 0) {
+      tol_s = static_cast<double>(n) * kEps * mx;
+      fail_s = -1;
+    }
   }
   __syncthreads();
   const double tol = tol_s;
