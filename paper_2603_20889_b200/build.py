@@ -20,8 +20,7 @@ SOURCES = ["tsqr_kernels.cu", "tsqr_thread_kernels.cu", "tsqr_group_kernels.cu",
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
     "-Xcompiler", "-fPIC", "-I", str(INCLUDE), "-I", str(CSRC),
-] + (["-DSQB_FOLD_EXPERIMENT"] if os.environ.get("SQB_FOLD_EXPERIMENT") else []) \
-  + (["-DSQB_FOLD_NOCHAIN"] if os.environ.get("SQB_FOLD_NOCHAIN") else [])
+] + (["-DSQB_FOLD_EXPERIMENT"] if os.environ.get("SQB_FOLD_EXPERIMENT") else [])  # extra (NS, G, P) variants for tuning
 
 
 def _nvcc() -> str:

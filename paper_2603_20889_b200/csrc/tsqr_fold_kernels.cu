@@ -148,11 +148,7 @@ struct Fold {
       }
       double sig = s0 + s1;
       if constexpr (G > 1) sig = __shfl_sync(0xffffffffu, sig, gn, G);
-#ifdef SQB_FOLD_NOCHAIN
-      hn.beta = sig; hn.u0 = tri[rowoff_next + c + 1]; hn.gamma = 1e-300 * sig;
-#else
       hn = make_reflector(tri[rowoff_next + c + 1], sig);
-#endif
     }
 #pragma unroll
     for (int i = 0; i < P; ++i) {
