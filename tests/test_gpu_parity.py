@@ -218,7 +218,7 @@ def test_svqb2_truncates_rank_deficient(ctx, oracle):
 
 
 @pytest.mark.parametrize("method", ["tsqr", "cholqr2", "svqb2"])
-@pytest.mark.parametrize("m,n", [(5000, 4), (20000, 15), (9000, 31)])
+@pytest.mark.parametrize("m,n", [(5000, 4), (7001, 8), (20000, 15), (12000, 28), (9000, 31), (8000, 63)])
 def test_solve_lstsq(ctx, oracle, method, m, n):
     a = gaussian(m, n, seed=n)
     rhs = a @ np.arange(1, n + 1, dtype=np.float64) + 0.01 * gaussian(m, 1, seed=77)[:, 0]
