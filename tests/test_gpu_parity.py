@@ -384,3 +384,29 @@ def test_every_tsqr_kernel_family(kind, oracle):
     env = dict(os.environ, SQB_TSQR_KERNEL=kind)
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("n", [8, 16, 32, 64])
+def test_full_size_self_consistency(ctx, n):
+    """BASELINE configs[1] at its real size (m = 2^27, up to 64 GiB resident): no CPU oracle fits there,
+    so parity is through size-independent properties - R^T R against the independently
+    computed Gram matrix, TSQR against CholQR2, and |(X R^-1)^T (X R^-1) - I| from the fused sweep."""
+    import torch
+    free, _ = torch.cuda.mem_get_info()
+    m = 1 << 27
+    if free < 8 * m * n + (4 << 30):
+        pytest.skip("not enough free HBM for the full-size matrix")
+    x = ctx.fill_gaussian(m, n, seed=1234)
+    r = ctx.tsqr_qless(x)
+    r2 = ctx.cholqr2(x)
+    c = ctx.tsmttsm(x)
+    g = ctx.tsmRttsmR(x, r)
+    ctx.synchronize()
+    rh, r2h, ch, gh = (t.cpu().numpy() for t in (r, r2, c, g))
+    xn2 = float(np.trace(ch))  # |X|_F^2
+    assert np.all(np.tril(rh, -1) == 0.0) and np.all(np.diag(rh) > 0.0)
+    assert np.linalg.norm(rh.T @ rh - ch) <= 50 * n * EPS * xn2
+    assert np.linalg.norm(rh - r2h) <= 64 * n * EPS * np.sqrt(xn2)
+    assert np.linalg.norm(gh - np.eye(n), 2) <= 1e-12
+    del x
+    torch.cuda.empty_cache()
