@@ -173,6 +173,21 @@ if clk.exists():
 tests = G / f"{tag}_gpu_tests.txt"
 if tests.exists():
     out.append(f"\n## GPU tests on the same box\n\n```\n{tests.read_text().strip()}\n```")
+alln = G / f"{tag}_all_n.txt"
+if alln.exists():
+    import re
+    shutil.copy(alln, P / f"{tag}_all_n.txt")
+    tab = {}
+    for l in open(alln):
+        mm = re.match(r"(\w+) n=\s*(\d+) m=\s*(\d+)\s+([\d.]+) ms\s+([\d.]+) GB/s", l)
+        if mm:
+            tab.setdefault(int(mm.group(2)), {})[mm.group(1)] = float(mm.group(5))
+    out.append(f"\n## Every column count 1..64 at 16 GiB of X ({tag}_all_n.txt; `tools/time_methods.py`), effective GB/s\n")
+    out.append("| n | TSQR | CholQR2 | SVQB2 | tsmttsm |")
+    out.append("|---|---|---|---|---|")
+    for nn in sorted(tab):
+        r = tab[nn]
+        out.append(f"| {nn} | {r.get('tsqr', 0):.0f} | {r.get('cholqr2', 0):.0f} | {r.get('svqb2', 0):.0f} | {r.get('tsmttsm', 0):.0f} |")
 san = G / f"{tag}_sanitizer.txt"
 if san.exists():
     out.append(f"\n## compute-sanitizer (memcheck on the GPU parity suite, racecheck on the Gram / TSQR parity tests)\n\n```\n{san.read_text().strip()}\n```")
