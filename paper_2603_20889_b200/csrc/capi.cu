@@ -202,6 +202,43 @@ int cholqr2_view(sqb_context* ctx, const MatView& v, long long m, int n, long lo
   return SQB_OK;
 }
 
+// ---- wide column counts (64 < n): plain Gram up to 256 columns, fused solve + Gram up to 128 ----
+int gram_wide_view(sqb_context* ctx, const double* d_x, long long m, int n, long long ld, int op,
+                   const double* factor, double* d_c, bool check) {
+  const size_t partial = gram_wide_partial_doubles(n, ctx->sm_count);
+  if (op == OP_PLAIN) {
+    if (n > kWideGramMaxN) return SQB_E_ARGUMENT;
+    SQB_TRY(grow(&ctx->work, &ctx->work_doubles, partial + gram_wide_solve_scratch_doubles()));
+    SQB_CUDA(launch_gram_wide(d_x, m, n, ld, ctx->sm_count, ctx->work, d_c, check ? 1 : 0, ctx->d_status,
+                              ctx->stream));
+    ctx->launches += 2;
+    return SQB_OK;
+  }
+  if (op != OP_SOLVE || n > kWideSolveMaxN) return SQB_E_ARGUMENT;
+  SQB_TRY(grow(&ctx->work, &ctx->work_doubles, partial + gram_wide_solve_scratch_doubles()));
+  SQB_CUDA(launch_gram_wide_solve(d_x, m, n, ld, factor, ctx->sm_count, ctx->work + partial, ctx->work, d_c,
+                                  ctx->d_status, ctx->stream));
+  ctx->launches += 3;
+  return SQB_OK;
+}
+
+// CholQR2 beyond 64 columns (the reference's cholqr2 has no column limit, gram_qr.cpp:123-131): the
+// wide SYRK, the one-CTA Cholesky (n <= 128), the fused solve + Gram sweep, Cholesky, R = R2 R1.
+int cholqr2_wide(sqb_context* ctx, const double* d_x, long long m, int n, long long ld, double* d_r,
+                 const std::function<int(double*)>& allreduce) {
+  Small s;
+  SQB_TRY(small_slots(ctx, n, &s));
+  SQB_TRY(gram_wide_view(ctx, d_x, m, n, ld, OP_PLAIN, nullptr, s.c1, true));
+  if (allreduce) SQB_TRY(allreduce(s.c1));
+  SQB_CUDA(launch_cholesky(s.c1, n, s.r1, ctx->d_status, ctx->stream));
+  SQB_TRY(gram_wide_view(ctx, d_x, m, n, ld, OP_SOLVE, s.r1, s.c2, false));
+  if (allreduce) SQB_TRY(allreduce(s.c2));
+  SQB_CUDA(launch_cholesky(s.c2, n, s.r2, ctx->d_status, ctx->stream));
+  SQB_CUDA(launch_tri_multiply(s.r2, s.r1, n, d_r, ctx->stream));
+  ctx->launches += 3;
+  return SQB_OK;
+}
+
 // SVQB2 (gram_qr.cpp:178-191): sigma from pass 1, rank from pass 2, B = B1 B2, Z = Z2 Z1.
 int svqb2_view(sqb_context* ctx, const MatView& v, long long m, int n, long long k, long long b,
                double* d_transform, double* d_z, double* d_sigma, long long* d_rank,
@@ -503,14 +540,9 @@ static int gram_entry(sqb_context* ctx, const double* d_x, int64_t m, int64_t n,
   if (n < 1 || m < 0) return SQB_E_DIMENSION;
   if (ld < m) return SQB_E_ARGUMENT;
   if (n > 64) {
-    // the reference's tsmttsm has no column limit (gram.cpp:113-121); the fused variants stay at
-    // n <= 64 here (register / shared-memory tiles), the plain Gram goes up to 256 columns
-    if (op != OP_PLAIN || n > kWideGramMaxN) return SQB_E_ARGUMENT;
-    const int nn = static_cast<int>(n);
-    SQB_TRY(grow(&ctx->work, &ctx->work_doubles, gram_wide_partial_doubles(nn, ctx->sm_count)));
-    SQB_CUDA(launch_gram_wide(d_x, m, nn, ld, ctx->sm_count, ctx->work, d_c, 1, ctx->d_status, ctx->stream));
-    ctx->launches += 2;
-    return SQB_OK;
+    // the reference's Gram kernels have no column limit (gram.cpp:113-151); here the plain Gram goes
+    // up to 256 columns and the fused solve + Gram up to 128; the fused multiply stays at n <= 64
+    return gram_wide_view(ctx, d_x, m, static_cast<int>(n), ld, op, factor, d_c, op == OP_PLAIN);
   }
   if (op == OP_MULTIPLY) {  // tsmmttsmm checks B for finiteness (gram.cpp:143-145)
     SQB_CUDA(launch_check_finite(factor, n * n, ctx->d_status, ctx->stream));
@@ -560,7 +592,8 @@ int sqb_eigh_small_dev(sqb_context* ctx, const double* d_c, int64_t n, double* d
 int sqb_cholqr2_dev(sqb_context* ctx, const double* d_x, int64_t m, int64_t n, int64_t ld,
                     int64_t num_blocks, int64_t panel_rows, double* d_r) {
   SQB_TRY(enter(ctx));
-  SQB_TRY(check_shape(m, n, ld, 64));
+  SQB_TRY(check_shape(m, n, ld, kWideSolveMaxN));
+  if (n > 64) return cholqr2_wide(ctx, d_x, m, static_cast<int>(n), ld, d_r, nullptr);
   return cholqr2_view(ctx, plain_view(d_x, ld, static_cast<int>(n)), m, static_cast<int>(n), num_blocks,
                       panel_rows, d_r, nullptr);
 }
@@ -706,7 +739,7 @@ static int gram_host(sqb_context* ctx, const double* x, int64_t m, int64_t n, in
                      const double* factor, int64_t k, int64_t b, double* c) {
   SQB_TRY(enter(ctx));
   if (n < 1 || m < 0) return SQB_E_DIMENSION;
-  if (n > (op == OP_PLAIN ? kWideGramMaxN : 64) || ld < m) return SQB_E_ARGUMENT;
+  if (n > (op == OP_PLAIN ? kWideGramMaxN : (op == OP_SOLVE ? kWideSolveMaxN : 64)) || ld < m) return SQB_E_ARGUMENT;
   const int nn = static_cast<int>(n);
   Small s;
   SQB_TRY(small_slots(ctx, nn, &s));
@@ -759,12 +792,13 @@ int sqb_eigh_small_host(sqb_context* ctx, const double* c, int64_t n, double* va
 int sqb_cholqr2_host(sqb_context* ctx, const double* x, int64_t m, int64_t n, int64_t ld,
                      int64_t num_blocks, int64_t panel_rows, double* r) {
   SQB_TRY(enter(ctx));
-  SQB_TRY(check_shape(m, n, ld, 64));
+  SQB_TRY(check_shape(m, n, ld, kWideSolveMaxN));
   const int nn = static_cast<int>(n);
   Small s;
   SQB_TRY(small_slots(ctx, nn, &s));
   SQB_TRY(upload_slabs(ctx, x, m, nn, ld, 2, nullptr));
-  SQB_TRY(cholqr2_view(ctx, plain_view(ctx->xbuf, m, nn), m, nn, num_blocks, panel_rows, s.rr, nullptr));
+  if (nn > 64) SQB_TRY(cholqr2_wide(ctx, ctx->xbuf, m, nn, m, s.rr, nullptr));
+  else SQB_TRY(cholqr2_view(ctx, plain_view(ctx->xbuf, m, nn), m, nn, num_blocks, panel_rows, s.rr, nullptr));
   SQB_TRY(download(ctx, r, s.rr, sizeof(double) * nn * nn));
   return sqb_sync(ctx);
 }
@@ -910,8 +944,10 @@ int sqb_cholqr2_sharded_dev(sqb_context* ctx, const double* d_x, int64_t m_local
                             int64_t ld, double* d_r) {
   SQB_TRY(enter(ctx));
   if (n < 1 || m_local < 0) return SQB_E_DIMENSION;
-  if (n > 64 || ld < m_local) return SQB_E_ARGUMENT;
+  if (n > kWideSolveMaxN || ld < m_local) return SQB_E_ARGUMENT;
   const int nn = static_cast<int>(n);
+  if (nn > 64)
+    return cholqr2_wide(ctx, d_x, m_local, nn, ld, d_r, [ctx, nn](double* d) { return allreduce_square(ctx, d, nn); });
   return cholqr2_view(ctx, plain_view(d_x, ld, nn), m_local, nn, 0, 0, d_r,
                       [ctx, nn](double* d) { return allreduce_square(ctx, d, nn); });
 }

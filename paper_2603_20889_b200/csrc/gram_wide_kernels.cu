@@ -54,14 +54,14 @@ __device__ __forceinline__ double2 frag(const double* stage, int tile, int t, in
 }
 
 // Triangular chunk, warp W: tile rows W and 15-W of the 16 x 16 upper block triangle.
-template <int W>
+template <int W, int PP = kTriP>
 __device__ __forceinline__ void tri_panel(const double* stage, double (&acc)[32][2], int g, int q) {
   constexpr int R1 = W, R2 = kWT - 1 - W;
 #pragma unroll
-  for (int t = 0; t < kTriP / 8; ++t) {
+  for (int t = 0; t < PP / 8; ++t) {
     double2 b[kWT - R1];
 #pragma unroll
-    for (int j = R1; j < kWT; ++j) b[j - R1] = frag<kTriP>(stage, j, t, g, q);
+    for (int j = R1; j < kWT; ++j) b[j - R1] = frag<PP>(stage, j, t, g, q);
     const double2 a1 = b[0], a2 = b[R2 - R1];
 #pragma unroll
     for (int j = R1; j < kWT; ++j) dmma_w(acc[j - R1][0], acc[j - R1][1], a1.x, b[j - R1].x);
@@ -238,6 +238,218 @@ __global__ void __launch_bounds__(kWThreads, 1) gram_wide_kernel(const WideParam
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// Fused solve + Gram for 64 < n <= 128: the second CholQR2 sweep, C2 = (X R^-1)^T (X R^-1), with no Q
+// write-back (reference tsmRttsmR -> blocked_gram(solve), src/gram.cpp:123-140, 57-62).
+//
+// The reference substitutes column by column inside a cache-resident panel; a column-sequential
+// substitution across 128 columns would serialise the eight warps of a CTA, so here the triangular
+// solve is turned into a tensor-core GEMM with the explicit inverse U = R^-1 (rinv_wide_kernel, one
+// CTA, 40 us): per 24-row panel
+//     Q^T tile (8 columns j x 8 rows)  =  sum_{k <= j}  U^T[8j.., 4k..] * X^T[4k.., rows]     (DMMA)
+// whose accumulator fragment (lane (g,q): Q[row 2q+e, column 8j+g]) is exactly the operand layout of
+// the SYRK (tri_panel), so it goes to a shared Q panel with one conflict-free 128-bit store and the
+// SYRK of gram_wide_kernel runs on it unchanged.  Warp w forms tile columns w and 15-w (34 k-steps,
+// the same balance as the SYRK's 17 tile pairs); its U fragments sit in shared memory in issue order.
+// The Q panel is double-buffered and the SYRK runs one panel behind the GEMM: one CTA barrier per
+// panel.  Same forward error class as the substitution (|dQ| <~ n eps |X| |R^-1|); deviation noted
+// in DESIGN.md.
+// ------------------------------------------------------------------------------------------------
+constexpr int kSolveP = 24;       // panel rows == pitch == 8 (mod 16)
+constexpr int kSolveKSteps = 34;  // k4 steps per warp: (2w+2) + (32-2w)
+constexpr int kSolveFragDoubles = 8 * kSolveKSteps * 32;
+constexpr double kEpsW = 2.220446049250313e-16;
+
+// U = R^-1 by back substitution, thread j owns column j; written in the fused kernel's fragment order:
+// warp w, step f (f < 2w+2: tile column w, k-step f; else tile column 15-w, k-step f-2w-2),
+// lane (g,q): U[4k+q, 8j+g].  Also the reference's pre-check |R(j,j)| > n eps max|diag| (gram.cpp:126-134).
+__global__ void __launch_bounds__(128, 1)
+    rinv_wide_kernel(const double* __restrict__ r, int n, double* __restrict__ frags, StatusWord* status) {
+  extern __shared__ __align__(16) double sm[];
+  double* rp = sm;                       // packed upper triangle of R
+  double* u = sm + tri_size(kWC);        // U[k * 128 + j]
+  __shared__ double mx_s;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < kWC * kWC; idx += 128) {
+    const int i = idx % kWC, j = idx / kWC;
+    if (i <= j) rp[tri_index(i, j)] = (j < n) ? r[i + static_cast<long long>(j) * n] : (i == j ? 1.0 : 0.0);
+    u[idx] = 0.0;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    double mx = 0.0;
+    for (int j = tid; j < n; j += 32) mx = fmax(mx, fabs(rp[tri_index(j, j)]));
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (tid == 0) mx_s = mx;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const double dtol = static_cast<double>(n) * kEpsW * mx_s;
+    for (int j = 0; j < n; ++j)
+      if (fabs(rp[tri_index(j, j)]) <= dtol) {
+        raise_status(status, SQB_E_SINGULAR, j);
+        break;
+      }
+  }
+  {  // row i of U needs rows i+1.. of U only in the own column: no barrier; i is warp-uniform so the
+     // R entries are broadcasts and the U reads are lane-contiguous
+    const int j = tid;
+    if (j < n) u[j * kWC + j] = 1.0 / rp[tri_index(j, j)];
+    for (int i = n - 2; i >= 0; --i) {
+      if (j > i && j < n) {
+        double s0 = 0.0, s1 = 0.0;
+        int k = i + 1;
+        for (; k + 1 <= j; k += 2) {
+          s0 = fma(rp[tri_index(i, k)], u[k * kWC + j], s0);
+          s1 = fma(rp[tri_index(i, k + 1)], u[(k + 1) * kWC + j], s1);
+        }
+        if (k <= j) s0 = fma(rp[tri_index(i, k)], u[k * kWC + j], s0);
+        u[i * kWC + j] = -(s0 + s1) / rp[tri_index(i, i)];
+      }
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < kSolveFragDoubles; idx += 128) {
+    const int lane = idx & 31, f = (idx >> 5) % kSolveKSteps, w = idx / (32 * kSolveKSteps);
+    const int g = lane >> 2, q = lane & 3;
+    const int j = f < 2 * w + 2 ? w : kWT - 1 - w;
+    const int kk = f < 2 * w + 2 ? f : f - (2 * w + 2);
+    const int row = 4 * kk + q, col = 8 * j + g;
+    frags[idx] = (row <= col && col < n) ? u[row * kWC + col] : 0.0;
+  }
+}
+
+// Q^T tiles of tile columns W and 15-W for the three row groups of a panel -> shared Q panel.
+template <int W>
+__device__ __forceinline__ void solve_panel(const double* stage, const double* rf, double* qb, int lane,
+                                            int g, int q) {
+  constexpr int J1 = W, J2 = kWT - 1 - W, K1 = 2 * J1 + 2, K2 = 2 * J2 + 2, NT = kSolveP / 8;
+  double a1c[NT][2], a2c[NT][2];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) a1c[t][0] = a1c[t][1] = a2c[t][0] = a2c[t][1] = 0.0;
+  const double* rfw = rf + W * kSolveKSteps * 32 + lane;
+#pragma unroll
+  for (int kk = 0; kk < K2; ++kk) {
+    double b[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) b[t] = stage[(4 * kk + q) * kSolveP + 8 * t + g];
+    const double a2 = rfw[(K1 + kk) * 32];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) dmma_w(a2c[t][0], a2c[t][1], a2, b[t]);
+    if (kk < K1) {
+      const double a1 = rfw[kk * 32];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) dmma_w(a1c[t][0], a1c[t][1], a1, b[t]);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    *reinterpret_cast<double2*>(qb + (8 * J1 + g) * kSolveP + 8 * t + 2 * q) = make_double2(a1c[t][0], a1c[t][1]);
+    *reinterpret_cast<double2*>(qb + (8 * J2 + g) * kSolveP + 8 * t + 2 * q) = make_double2(a2c[t][0], a2c[t][1]);
+  }
+}
+
+struct WideSolveParams {
+  const double* x;
+  long long ld, m;
+  int n, kb;
+  const double* frags;  // U = R^-1 in fragment order (rinv_wide_kernel)
+  double* partial;      // one 128 x 128 column-major slab per CTA
+};
+
+__global__ void __launch_bounds__(kWThreads, 1) gram_wide_solve_kernel(const WideSolveParams prm) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ uint64_t bars[kWStages];
+  constexpr int kStageDoubles = kWC * kSolveP;
+  double* qbuf = smem + kWStages * kStageDoubles;  // two Q panels
+  double* rf = qbuf + 2 * kStageDoubles;           // U fragments
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int rb = blockIdx.x;
+
+  const int slot = tid;
+  const bool slot_ok = slot < kWC && slot < prm.n;
+  const int valid_slots = prm.n < kWC ? prm.n : kWC;
+
+  for (int i = tid; i < (kWStages + 2) * kStageDoubles; i += kWThreads) smem[i] = 0.0;
+  for (int i = tid; i < kSolveFragDoubles; i += kWThreads) rf[i] = prm.frags[i];
+  if (tid < kWStages) mbar_init(&bars[tid], 1);
+  mbar_fence_init();
+  __syncthreads();
+
+  long long rpb = (prm.m + prm.kb - 1) / prm.kb;
+  rpb = (rpb + kSolveP - 1) / kSolveP * kSolveP;
+  const long long begin = min(static_cast<long long>(rb) * rpb, prm.m);
+  const long long end = min(static_cast<long long>(rb + 1) * rpb, prm.m);
+  const long long npanels = (end - begin + kSolveP - 1) / kSolveP;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(prm.x) & 15) == 0) && ((prm.ld & 1) == 0);
+  const double* colp = prm.x + static_cast<long long>(slot_ok ? slot : 0) * prm.ld;
+
+  double acc[32][2];
+#pragma unroll
+  for (int p = 0; p < 32; ++p) acc[p][0] = acc[p][1] = 0.0;
+
+  uint32_t phase_bits = 0, async_bits = 0;
+  auto will_be_async = [&](long long pn) { return aligned && begin + pn * kSolveP + kSolveP <= end; };
+  auto fill = [&](long long pn, int s) {
+    const long long r0 = begin + pn * kSolveP;
+    double* st = smem + s * kStageDoubles;
+    if (will_be_async(pn)) {
+      if (slot_ok) {
+        fence_async_smem();
+        bulk_g2s(st + slot * kSolveP, colp + r0, kSolveP * sizeof(double), &bars[s]);
+      }
+      async_bits |= 1u << s;
+    } else {
+      if (slot_ok) {
+        for (int r = 0; r < kSolveP; ++r) st[slot * kSolveP + r] = (r0 + r < end) ? __ldg(colp + r0 + r) : 0.0;
+      }
+      async_bits &= ~(1u << s);
+    }
+  };
+  const uint32_t tx_bytes = static_cast<uint32_t>(valid_slots * kSolveP * sizeof(double));
+
+  if (tid == 0) {
+    for (int s = 0; s < kWStages - 1; ++s)
+      if (s < npanels && will_be_async(s)) mbar_expect_tx(&bars[s], tx_bytes);
+  }
+  __syncthreads();
+  for (int s = 0; s < kWStages - 1; ++s)
+    if (s < npanels) fill(s, s);
+
+  // iteration pn: SYRK of panel pn-1 (from its Q panel), then the solve GEMM of panel pn
+  for (long long pn = 0; pn <= npanels; ++pn) {
+    const int s = static_cast<int>(pn % kWStages);
+    const long long nxt = pn + kWStages - 1;
+    const int sn = static_cast<int>(nxt % kWStages);
+    if (tid == 0 && nxt < npanels && will_be_async(nxt)) mbar_expect_tx(&bars[sn], tx_bytes);
+    __syncthreads();  // GEMM(pn-1) done everywhere: stage sn free, Q panel (pn-1)&1 complete; SYRK(pn-2) done
+    if (nxt < npanels) fill(nxt, sn);
+    if (pn > 0) {
+      const double* qp = qbuf + ((pn - 1) & 1) * kStageDoubles;
+#define SQB_TRI(WV) tri_panel<WV, kSolveP>(qp, acc, g, q)
+      SQB_WARP_SWITCH(SQB_TRI)
+#undef SQB_TRI
+    }
+    if (pn < npanels) {
+      if (async_bits & (1u << s)) {
+        mbar_wait(&bars[s], (phase_bits >> s) & 1u);
+        phase_bits ^= 1u << s;
+      }
+      const double* stage = smem + s * kStageDoubles;
+      double* qp = qbuf + (pn & 1) * kStageDoubles;
+#define SQB_SOLVE(WV) solve_panel<WV>(stage, rf, qp, lane, g, q)
+      SQB_WARP_SWITCH(SQB_SOLVE)
+#undef SQB_SOLVE
+    }
+  }
+
+  double* dst = prm.partial + static_cast<long long>(blockIdx.x) * kWC * kWC;
+#define SQB_TRIS(WV) tri_store<WV>(dst, acc, g, q)
+  SQB_WARP_SWITCH(SQB_TRIS)
+#undef SQB_TRIS
+}
+
 // Sum the row-block partials of every chunk in ascending block order, mirror (gram.cpp:81-92).
 __global__ void gram_wide_reduce_kernel(const double* partial, int kb_tri, int kb_full, int n, double* c,
                                         int check_finite, StatusWord* status) {
@@ -302,6 +514,43 @@ cudaError_t launch_gram_wide(const double* x, long long m, int n, long long ld, 
   if (e != cudaSuccess) return e;
   gram_wide_reduce_kernel<<<(n * n + 255) / 256, 256, 0, stream>>>(partial, prm.kb_tri, prm.kb_full, n, c,
                                                                    check_finite, status);
+  return cudaGetLastError();
+}
+
+size_t gram_wide_solve_scratch_doubles() { return kSolveFragDoubles; }
+
+cudaError_t launch_gram_wide_solve(const double* x, long long m, int n, long long ld, const double* r,
+                                   int sm_count, double* frags, double* partial, double* c, StatusWord* status,
+                                   cudaStream_t stream) {
+  if (n <= 64 || n > kWideSolveMaxN) return cudaErrorInvalidValue;
+  static bool configured = false;
+  const size_t rinv_bytes = sizeof(double) * (tri_size(kWC) + kWC * kWC);
+  const size_t bytes = sizeof(double) * ((kWStages + 2) * kWC * kSolveP + kSolveFragDoubles);
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(rinv_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(rinv_bytes));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(gram_wide_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(bytes));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  rinv_wide_kernel<<<1, 128, rinv_bytes, stream>>>(r, n, frags, status);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  WideSolveParams prm;
+  prm.x = x;
+  prm.ld = ld;
+  prm.m = m;
+  prm.n = n;
+  prm.frags = frags;
+  prm.partial = partial;
+  const long long panels = (m + kSolveP - 1) / kSolveP;
+  prm.kb = static_cast<int>(panels < sm_count ? (panels > 0 ? panels : 1) : sm_count);
+  gram_wide_solve_kernel<<<prm.kb, kWThreads, bytes, stream>>>(prm);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  gram_wide_reduce_kernel<<<(n * n + 255) / 256, 256, 0, stream>>>(partial, prm.kb, 0, n, c, 0, status);
   return cudaGetLastError();
 }
 

@@ -147,15 +147,73 @@ def test_wide_gram(ctx, sq, oracle, m, n):
     cu = ctx.tsmttsm(big.t()[1:m + 1, :])
     ctx.synchronize()
     assert np.linalg.norm(cu.cpu().numpy() - c_ref) <= 5 * n * EPS * xn2
-    # the fused variants keep the n <= 64 limit; tsmttsm stops at 256 columns
+    # the fused multiply keeps the n <= 64 limit, the fused solve stops at 128 columns, tsmttsm at 256
     with pytest.raises(sq.ArgumentError):
-        ctx.tsmRttsmR(x, np.eye(n))
+        ctx.tsmmttsmm(x, np.eye(n))
+    if n > 128:
+        with pytest.raises(sq.ArgumentError):
+            ctx.tsmRttsmR(x, np.eye(n))
     x[m // 2, n - 1] = np.inf
     with pytest.raises(sq.ArgumentError):
         ctx.tsmttsm(x)
 
 
+@pytest.mark.parametrize("m,n", [(4000, 65), (5003, 100), (9000, 128), (20011, 127), (300, 128), (128, 128)])
+def test_wide_solve_gram_and_cholqr2(ctx, sq, oracle, m, n):
+    """64 < n <= 128: the reference's tsmRttsmR / cholqr2 have no column limit (gram.cpp:123-140,
+    gram_qr.cpp:123-131); fused solve + Gram DMMA kernel (explicit R^-1 GEMM feeding the SYRK) against
+    the oracle, host and device entry points, aligned and unaligned staging, error parity."""
+    import torch
+    x = gaussian(m, n, seed=5 * n + m)
+    c_ref = oracle.port.tsmttsm(x)
+    r1 = np.linalg.cholesky(c_ref).T.copy(order="F")
+    c2_ref = oracle.port.tsmRttsmR(x, r1)
+    c2 = ctx.tsmRttsmR(x, r1)
+    assert np.array_equal(c2, c2.T)
+    assert np.linalg.norm(c2 - c2_ref) <= 50 * n * EPS * n
+    assert np.linalg.norm(c2 - np.eye(n)) <= 1e-10 * np.linalg.cond(r1)
+    xd = torch.from_numpy(np.ascontiguousarray(x.T)).cuda().t()
+    c2d = ctx.tsmRttsmR(xd, torch.from_numpy(np.ascontiguousarray(r1.T)).cuda().t())
+    ctx.synchronize()
+    assert np.linalg.norm(c2d.cpu().numpy() - c2_ref) <= 50 * n * EPS * n
+    big = torch.zeros((n, m + 3), dtype=torch.float64, device="cuda")
+    big[:, 1:m + 1] = xd.t()
+    c2u = ctx.tsmRttsmR(big.t()[1:m + 1, :], torch.from_numpy(np.ascontiguousarray(r1.T)).cuda().t())
+    ctx.synchronize()
+    assert np.linalg.norm(c2u.cpu().numpy() - c2_ref) <= 50 * n * EPS * n
+    # a general (non-Cholesky) upper factor with a graded diagonal
+    rg = np.triu(gaussian(n, n, seed=n)) / np.sqrt(n) + np.diag(np.linspace(1.0, 3.0, n))
+    rg = np.asfortranarray(rg)
+    cg = ctx.tsmRttsmR(x, rg)
+    cg_ref = oracle.port.tsmRttsmR(x, rg)
+    assert np.linalg.norm(cg - cg_ref) <= 50 * n * EPS * np.linalg.norm(cg_ref) * np.linalg.cond(rg)
+    # CholQR2
+    xn = np.linalg.norm(x)
+    r = ctx.cholqr2(x)
+    r_ref = oracle.port.cholqr2(x)
+    assert np.all(np.tril(r, -1) == 0.0) and np.all(np.diag(r) > 0.0)
+    assert np.linalg.norm(r - r_ref) <= 64 * n * EPS * xn
+    assert np.linalg.norm(r.T @ r - c_ref) <= 50 * n * EPS * xn ** 2
+    rd = ctx.cholqr2(xd)
+    ctx.synchronize()
+    assert np.linalg.norm(rd.cpu().numpy() - r_ref) <= 64 * n * EPS * xn
+    # error parity: singular factor (gram.cpp:126-134) and Cholesky breakdown (gram_qr.cpp:39-54)
+    rs = r1.copy(order="F")
+    rs[n // 2, n // 2] = 0.0
+    with pytest.raises(sq.SingularFactorError) as ei:
+        ctx.tsmRttsmR(x, rs)
+    assert ei.value.diagonal_index == n // 2
+    xb = x.copy(order="F")
+    xb[:, n - 1] = xb[:, 0]
+    with pytest.raises(sq.BreakdownError):
+        ctx.cholqr2(xb)
+    r_again = ctx.cholqr2(x)
+    assert np.array_equal(r_again, r)
+
+
 def test_wide_gram_limit(ctx, sq):
+    with pytest.raises(sq.ArgumentError):
+        ctx.cholqr2(gaussian(300, 129))
     with pytest.raises(sq.ArgumentError):
         ctx.tsmttsm(gaussian(300, 257))
 
