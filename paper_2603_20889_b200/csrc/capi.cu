@@ -208,15 +208,15 @@ int gram_wide_view(sqb_context* ctx, const double* d_x, long long m, int n, long
   const size_t partial = gram_wide_partial_doubles(n, ctx->sm_count);
   if (op == OP_PLAIN) {
     if (n > kWideGramMaxN) return SQB_E_ARGUMENT;
-    SQB_TRY(grow(&ctx->work, &ctx->work_doubles, partial + gram_wide_solve_scratch_doubles()));
+    SQB_TRY(grow(&ctx->work, &ctx->work_doubles, partial + gram_wide_fused_scratch_doubles()));
     SQB_CUDA(launch_gram_wide(d_x, m, n, ld, ctx->sm_count, ctx->work, d_c, check ? 1 : 0, ctx->d_status,
                               ctx->stream));
     ctx->launches += 2;
     return SQB_OK;
   }
-  if (op != OP_SOLVE || n > kWideSolveMaxN) return SQB_E_ARGUMENT;
-  SQB_TRY(grow(&ctx->work, &ctx->work_doubles, partial + gram_wide_solve_scratch_doubles()));
-  SQB_CUDA(launch_gram_wide_solve(d_x, m, n, ld, factor, ctx->sm_count, ctx->work + partial, ctx->work, d_c,
+  if (n > kWideFusedMaxN) return SQB_E_ARGUMENT;
+  SQB_TRY(grow(&ctx->work, &ctx->work_doubles, partial + gram_wide_fused_scratch_doubles()));
+  SQB_CUDA(launch_gram_wide_fused(d_x, m, n, ld, op, factor, ctx->sm_count, ctx->work + partial, ctx->work, d_c,
                                   ctx->d_status, ctx->stream));
   ctx->launches += 3;
   return SQB_OK;
@@ -236,6 +236,23 @@ int cholqr2_wide(sqb_context* ctx, const double* d_x, long long m, int n, long l
   SQB_CUDA(launch_cholesky(s.c2, n, s.r2, ctx->d_status, ctx->stream));
   SQB_CUDA(launch_tri_multiply(s.r2, s.r1, n, d_r, ctx->stream));
   ctx->launches += 3;
+  return SQB_OK;
+}
+
+// SVQB2 beyond 64 columns (up to the reference's own eigh_small limit of 128, gram_qr.cpp:62).
+int svqb2_wide(sqb_context* ctx, const double* d_x, long long m, int n, long long ld, double* d_transform,
+               double* d_z, double* d_sigma, long long* d_rank, const std::function<int(double*)>& allreduce) {
+  Small s;
+  SQB_TRY(small_slots(ctx, n, &s));
+  SQB_TRY(gram_wide_view(ctx, d_x, m, n, ld, OP_PLAIN, nullptr, s.c1, true));
+  if (allreduce) SQB_TRY(allreduce(s.c1));
+  SQB_CUDA(launch_svqb_pass(s.c1, n, s.b1, s.z1, d_sigma, s.rank1, 1, s.scratch, ctx->d_status, ctx->stream));
+  SQB_TRY(gram_wide_view(ctx, d_x, m, n, ld, OP_MULTIPLY, s.b1, s.c2, false));
+  if (allreduce) SQB_TRY(allreduce(s.c2));
+  SQB_CUDA(launch_svqb_pass(s.c2, n, s.b2, s.z2, s.s2, d_rank, 0, s.scratch, ctx->d_status, ctx->stream));
+  SQB_CUDA(launch_small_multiply(s.b1, s.b2, n, d_transform, ctx->stream));
+  SQB_CUDA(launch_small_multiply(s.z2, s.z1, n, d_z, ctx->stream));
+  ctx->launches += 4;
   return SQB_OK;
 }
 
@@ -592,7 +609,7 @@ int sqb_eigh_small_dev(sqb_context* ctx, const double* d_c, int64_t n, double* d
 int sqb_cholqr2_dev(sqb_context* ctx, const double* d_x, int64_t m, int64_t n, int64_t ld,
                     int64_t num_blocks, int64_t panel_rows, double* d_r) {
   SQB_TRY(enter(ctx));
-  SQB_TRY(check_shape(m, n, ld, kWideSolveMaxN));
+  SQB_TRY(check_shape(m, n, ld, kWideFusedMaxN));
   if (n > 64) return cholqr2_wide(ctx, d_x, m, static_cast<int>(n), ld, d_r, nullptr);
   return cholqr2_view(ctx, plain_view(d_x, ld, static_cast<int>(n)), m, static_cast<int>(n), num_blocks,
                       panel_rows, d_r, nullptr);
@@ -602,7 +619,10 @@ int sqb_svqb2_dev(sqb_context* ctx, const double* d_x, int64_t m, int64_t n, int
                   int64_t num_blocks, int64_t panel_rows, double* d_transform, double* d_z,
                   double* d_sigma, int64_t* d_rank) {
   SQB_TRY(enter(ctx));
-  SQB_TRY(check_shape(m, n, ld, 64));
+  SQB_TRY(check_shape(m, n, ld, kWideFusedMaxN));
+  if (n > 64)
+    return svqb2_wide(ctx, d_x, m, static_cast<int>(n), ld, d_transform, d_z, d_sigma,
+                      reinterpret_cast<long long*>(d_rank), nullptr);
   return svqb2_view(ctx, plain_view(d_x, ld, static_cast<int>(n)), m, static_cast<int>(n), num_blocks,
                     panel_rows, d_transform, d_z, d_sigma, reinterpret_cast<long long*>(d_rank),
                     nullptr);
@@ -739,7 +759,7 @@ static int gram_host(sqb_context* ctx, const double* x, int64_t m, int64_t n, in
                      const double* factor, int64_t k, int64_t b, double* c) {
   SQB_TRY(enter(ctx));
   if (n < 1 || m < 0) return SQB_E_DIMENSION;
-  if (n > (op == OP_PLAIN ? kWideGramMaxN : (op == OP_SOLVE ? kWideSolveMaxN : 64)) || ld < m) return SQB_E_ARGUMENT;
+  if (n > (op == OP_PLAIN ? kWideGramMaxN : kWideFusedMaxN) || ld < m) return SQB_E_ARGUMENT;
   const int nn = static_cast<int>(n);
   Small s;
   SQB_TRY(small_slots(ctx, nn, &s));
@@ -792,7 +812,7 @@ int sqb_eigh_small_host(sqb_context* ctx, const double* c, int64_t n, double* va
 int sqb_cholqr2_host(sqb_context* ctx, const double* x, int64_t m, int64_t n, int64_t ld,
                      int64_t num_blocks, int64_t panel_rows, double* r) {
   SQB_TRY(enter(ctx));
-  SQB_TRY(check_shape(m, n, ld, kWideSolveMaxN));
+  SQB_TRY(check_shape(m, n, ld, kWideFusedMaxN));
   const int nn = static_cast<int>(n);
   Small s;
   SQB_TRY(small_slots(ctx, nn, &s));
@@ -823,14 +843,17 @@ int sqb_svqb2_host(sqb_context* ctx, const double* x, int64_t m, int64_t n, int6
                    int64_t num_blocks, int64_t panel_rows, double* transform, double* z,
                    double* sigma, int64_t* rank) {
   SQB_TRY(enter(ctx));
-  SQB_TRY(check_shape(m, n, ld, 64));
+  SQB_TRY(check_shape(m, n, ld, kWideFusedMaxN));
   const int nn = static_cast<int>(n);
   const size_t sq = static_cast<size_t>(nn) * nn;
   Small s;
   SQB_TRY(small_slots(ctx, nn, &s));
   SQB_TRY(upload_slabs(ctx, x, m, nn, ld, 2, nullptr));
-  SQB_TRY(svqb2_view(ctx, plain_view(ctx->xbuf, m, nn), m, nn, num_blocks, panel_rows, s.rr, s.rr + sq,
-                     s.s2 + nn, s.rank1 + 1, nullptr));
+  if (nn > 64)
+    SQB_TRY(svqb2_wide(ctx, ctx->xbuf, m, nn, m, s.rr, s.rr + sq, s.s2 + nn, s.rank1 + 1, nullptr));
+  else
+    SQB_TRY(svqb2_view(ctx, plain_view(ctx->xbuf, m, nn), m, nn, num_blocks, panel_rows, s.rr, s.rr + sq,
+                       s.s2 + nn, s.rank1 + 1, nullptr));
   SQB_TRY(download(ctx, transform, s.rr, sizeof(double) * sq));
   SQB_TRY(download(ctx, z, s.rr + sq, sizeof(double) * sq));
   SQB_TRY(download(ctx, sigma, s.s2 + nn, sizeof(double) * nn));
@@ -944,7 +967,7 @@ int sqb_cholqr2_sharded_dev(sqb_context* ctx, const double* d_x, int64_t m_local
                             int64_t ld, double* d_r) {
   SQB_TRY(enter(ctx));
   if (n < 1 || m_local < 0) return SQB_E_DIMENSION;
-  if (n > kWideSolveMaxN || ld < m_local) return SQB_E_ARGUMENT;
+  if (n > kWideFusedMaxN || ld < m_local) return SQB_E_ARGUMENT;
   const int nn = static_cast<int>(n);
   if (nn > 64)
     return cholqr2_wide(ctx, d_x, m_local, nn, ld, d_r, [ctx, nn](double* d) { return allreduce_square(ctx, d, nn); });
@@ -957,8 +980,11 @@ int sqb_svqb2_sharded_dev(sqb_context* ctx, const double* d_x, int64_t m_local, 
                           int64_t* d_rank) {
   SQB_TRY(enter(ctx));
   if (n < 1 || m_local < 0) return SQB_E_DIMENSION;
-  if (n > 64 || ld < m_local) return SQB_E_ARGUMENT;
+  if (n > kWideFusedMaxN || ld < m_local) return SQB_E_ARGUMENT;
   const int nn = static_cast<int>(n);
+  if (nn > 64)
+    return svqb2_wide(ctx, d_x, m_local, nn, ld, d_transform, d_z, d_sigma, reinterpret_cast<long long*>(d_rank),
+                      [ctx, nn](double* d) { return allreduce_square(ctx, d, nn); });
   return svqb2_view(ctx, plain_view(d_x, ld, nn), m_local, nn, 0, 0, d_transform, d_z, d_sigma,
                     reinterpret_cast<long long*>(d_rank),
                     [ctx, nn](double* d) { return allreduce_square(ctx, d, nn); });

@@ -256,9 +256,45 @@ __global__ void __launch_bounds__(kWThreads, 1) gram_wide_kernel(const WideParam
 // in DESIGN.md.
 // ------------------------------------------------------------------------------------------------
 constexpr int kSolveP = 24;       // panel rows == pitch == 8 (mod 16)
-constexpr int kSolveKSteps = 34;  // k4 steps per warp: (2w+2) + (32-2w)
-constexpr int kSolveFragDoubles = 8 * kSolveKSteps * 32;
+// k4 steps per warp: triangular factor (OP_SOLVE, U = R^-1) (2w+2) + (32-2w) = 34; dense factor
+// (OP_MULTIPLY, B) 32 + 32
+__host__ __device__ constexpr int fused_ksteps(int op) { return op == OP_SOLVE ? 34 : 64; }
+__host__ __device__ constexpr int fused_k1(int op, int w) { return op == OP_SOLVE ? 2 * w + 2 : 32; }
+__host__ __device__ constexpr int fused_k2(int op, int w) { return op == OP_SOLVE ? 2 * (kWT - 1 - w) + 2 : 32; }
+__host__ __device__ constexpr int fused_frag_doubles(int op) { return 8 * fused_ksteps(op) * 32; }
+// panels in flight: the fused passes are far on the tensor-pipe side (a panel is ~5 us of DMMAs), so the
+// dense factor's 128 KB of fragments may squeeze the ring down to two stages
+__host__ __device__ constexpr int fused_stages(int op) { return op == OP_SOLVE ? 4 : 2; }
 constexpr double kEpsW = 2.220446049250313e-16;
+
+// Factor element held by lane (g,q) of warp w at issue step f: tile column w for the first k1 steps,
+// tile column 15-w after; row 4k+q, column 8j+g.
+template <int OP>
+__device__ __forceinline__ void fused_frag_coord(int idx, int* row, int* col) {
+  const int lane = idx & 31, f = (idx >> 5) % fused_ksteps(OP), w = idx / (32 * fused_ksteps(OP));
+  const int g = lane >> 2, q = lane & 3;
+  const int k1 = fused_k1(OP, w);
+  const int j = f < k1 ? w : kWT - 1 - w;
+  const int kk = f < k1 ? f : f - k1;
+  *row = 4 * kk + q;
+  *col = 8 * j + g;
+}
+
+// OP_MULTIPLY: B (n x n, dense) into fragment order; tsmmttsmm validates B (gram.cpp:143-145).
+__global__ void bfrag_wide_kernel(const double* __restrict__ b, int n, double* __restrict__ frags,
+                                  StatusWord* status) {
+  for (int idx = threadIdx.x + blockIdx.x * blockDim.x; idx < fused_frag_doubles(OP_MULTIPLY);
+       idx += blockDim.x * gridDim.x) {
+    int row, col;
+    fused_frag_coord<OP_MULTIPLY>(idx, &row, &col);
+    double v = 0.0;
+    if (row < n && col < n) {
+      v = b[row + static_cast<long long>(col) * n];
+      if (is_nonfinite(v)) atomicExch(&status->nonfinite, 1);
+    }
+    frags[idx] = v;
+  }
+}
 
 // U = R^-1 by back substitution, thread j owns column j; written in the fused kernel's fragment order:
 // warp w, step f (f < 2w+2: tile column w, k-step f; else tile column 15-w, k-step f-2w-2),
@@ -309,25 +345,22 @@ __global__ void __launch_bounds__(128, 1)
     }
   }
   __syncthreads();
-  for (int idx = tid; idx < kSolveFragDoubles; idx += 128) {
-    const int lane = idx & 31, f = (idx >> 5) % kSolveKSteps, w = idx / (32 * kSolveKSteps);
-    const int g = lane >> 2, q = lane & 3;
-    const int j = f < 2 * w + 2 ? w : kWT - 1 - w;
-    const int kk = f < 2 * w + 2 ? f : f - (2 * w + 2);
-    const int row = 4 * kk + q, col = 8 * j + g;
+  for (int idx = tid; idx < fused_frag_doubles(OP_SOLVE); idx += 128) {
+    int row, col;
+    fused_frag_coord<OP_SOLVE>(idx, &row, &col);
     frags[idx] = (row <= col && col < n) ? u[row * kWC + col] : 0.0;
   }
 }
 
 // Q^T tiles of tile columns W and 15-W for the three row groups of a panel -> shared Q panel.
-template <int W>
+template <int W, int OP>
 __device__ __forceinline__ void solve_panel(const double* stage, const double* rf, double* qb, int lane,
                                             int g, int q) {
-  constexpr int J1 = W, J2 = kWT - 1 - W, K1 = 2 * J1 + 2, K2 = 2 * J2 + 2, NT = kSolveP / 8;
+  constexpr int J1 = W, J2 = kWT - 1 - W, K1 = fused_k1(OP, W), K2 = fused_k2(OP, W), NT = kSolveP / 8;
   double a1c[NT][2], a2c[NT][2];
 #pragma unroll
   for (int t = 0; t < NT; ++t) a1c[t][0] = a1c[t][1] = a2c[t][0] = a2c[t][1] = 0.0;
-  const double* rfw = rf + W * kSolveKSteps * 32 + lane;
+  const double* rfw = rf + W * fused_ksteps(OP) * 32 + lane;
 #pragma unroll
   for (int kk = 0; kk < K2; ++kk) {
     double b[NT];
@@ -353,12 +386,14 @@ struct WideSolveParams {
   const double* x;
   long long ld, m;
   int n, kb;
-  const double* frags;  // U = R^-1 in fragment order (rinv_wide_kernel)
+  const double* frags;  // U = R^-1 (rinv_wide_kernel) or B (bfrag_wide_kernel) in fragment order
   double* partial;      // one 128 x 128 column-major slab per CTA
 };
 
-__global__ void __launch_bounds__(kWThreads, 1) gram_wide_solve_kernel(const WideSolveParams prm) {
+template <int OP>
+__global__ void __launch_bounds__(kWThreads, 1) gram_wide_fused_kernel(const WideSolveParams prm) {
   extern __shared__ __align__(128) double smem[];
+  constexpr int kWStages = fused_stages(OP);  // shadows the plain kernel's ring depth
   __shared__ uint64_t bars[kWStages];
   constexpr int kStageDoubles = kWC * kSolveP;
   double* qbuf = smem + kWStages * kStageDoubles;  // two Q panels
@@ -372,7 +407,7 @@ __global__ void __launch_bounds__(kWThreads, 1) gram_wide_solve_kernel(const Wid
   const int valid_slots = prm.n < kWC ? prm.n : kWC;
 
   for (int i = tid; i < (kWStages + 2) * kStageDoubles; i += kWThreads) smem[i] = 0.0;
-  for (int i = tid; i < kSolveFragDoubles; i += kWThreads) rf[i] = prm.frags[i];
+  for (int i = tid; i < fused_frag_doubles(OP); i += kWThreads) rf[i] = prm.frags[i];
   if (tid < kWStages) mbar_init(&bars[tid], 1);
   mbar_fence_init();
   __syncthreads();
@@ -438,7 +473,7 @@ __global__ void __launch_bounds__(kWThreads, 1) gram_wide_solve_kernel(const Wid
       }
       const double* stage = smem + s * kStageDoubles;
       double* qp = qbuf + (pn & 1) * kStageDoubles;
-#define SQB_SOLVE(WV) solve_panel<WV>(stage, rf, qp, lane, g, q)
+#define SQB_SOLVE(WV) solve_panel<WV, OP>(stage, rf, qp, lane, g, q)
       SQB_WARP_SWITCH(SQB_SOLVE)
 #undef SQB_SOLVE
     }
@@ -517,26 +552,41 @@ cudaError_t launch_gram_wide(const double* x, long long m, int n, long long ld, 
   return cudaGetLastError();
 }
 
-size_t gram_wide_solve_scratch_doubles() { return kSolveFragDoubles; }
+size_t gram_wide_fused_scratch_doubles() { return fused_frag_doubles(OP_MULTIPLY); }
 
-cudaError_t launch_gram_wide_solve(const double* x, long long m, int n, long long ld, const double* r,
-                                   int sm_count, double* frags, double* partial, double* c, StatusWord* status,
-                                   cudaStream_t stream) {
-  if (n <= 64 || n > kWideSolveMaxN) return cudaErrorInvalidValue;
+template <int OP>
+static cudaError_t launch_fused(const WideSolveParams& prm, cudaStream_t stream) {
+  const size_t bytes = sizeof(double) * ((fused_stages(OP) + 2) * kWC * kSolveP + fused_frag_doubles(OP));
   static bool configured = false;
-  const size_t rinv_bytes = sizeof(double) * (tri_size(kWC) + kWC * kWC);
-  const size_t bytes = sizeof(double) * ((kWStages + 2) * kWC * kSolveP + kSolveFragDoubles);
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(rinv_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(rinv_bytes));
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(gram_wide_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(bytes));
+    cudaError_t e = cudaFuncSetAttribute(gram_wide_fused_kernel<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(bytes));
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  rinv_wide_kernel<<<1, 128, rinv_bytes, stream>>>(r, n, frags, status);
-  cudaError_t e = cudaGetLastError();
+  gram_wide_fused_kernel<OP><<<prm.kb, kWThreads, bytes, stream>>>(prm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gram_wide_fused(const double* x, long long m, int n, long long ld, int op, const double* factor,
+                                   int sm_count, double* frags, double* partial, double* c, StatusWord* status,
+                                   cudaStream_t stream) {
+  if (n <= 64 || n > kWideFusedMaxN || (op != OP_SOLVE && op != OP_MULTIPLY)) return cudaErrorInvalidValue;
+  cudaError_t e;
+  if (op == OP_SOLVE) {
+    static bool configured = false;
+    const size_t rinv_bytes = sizeof(double) * (tri_size(kWC) + kWC * kWC);
+    if (!configured) {
+      e = cudaFuncSetAttribute(rinv_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(rinv_bytes));
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+    rinv_wide_kernel<<<1, 128, rinv_bytes, stream>>>(factor, n, frags, status);
+  } else {
+    bfrag_wide_kernel<<<16, 256, 0, stream>>>(factor, n, frags, status);
+  }
+  e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   WideSolveParams prm;
   prm.x = x;
@@ -547,8 +597,7 @@ cudaError_t launch_gram_wide_solve(const double* x, long long m, int n, long lon
   prm.partial = partial;
   const long long panels = (m + kSolveP - 1) / kSolveP;
   prm.kb = static_cast<int>(panels < sm_count ? (panels > 0 ? panels : 1) : sm_count);
-  gram_wide_solve_kernel<<<prm.kb, kWThreads, bytes, stream>>>(prm);
-  e = cudaGetLastError();
+  e = op == OP_SOLVE ? launch_fused<OP_SOLVE>(prm, stream) : launch_fused<OP_MULTIPLY>(prm, stream);
   if (e != cudaSuccess) return e;
   gram_wide_reduce_kernel<<<(n * n + 255) / 256, 256, 0, stream>>>(partial, prm.kb, 0, n, c, 0, status);
   return cudaGetLastError();

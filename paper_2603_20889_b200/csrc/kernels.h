@@ -122,10 +122,11 @@ size_t gram_wide_partial_doubles(int n, int sm_count);
 cudaError_t launch_gram_wide(const double* x, long long m, int n, long long ld, int sm_count, double* partial,
                              double* c, int check_finite, StatusWord* status, cudaStream_t stream);
 
-// fused solve + Gram (the second CholQR2 sweep) for 64 < n <= 128; frags: gram_wide_solve_scratch_doubles()
-constexpr int kWideSolveMaxN = 128;
-size_t gram_wide_solve_scratch_doubles();
-cudaError_t launch_gram_wide_solve(const double* x, long long m, int n, long long ld, const double* r,
+// fused solve / multiply + Gram (the second CholQR2 / SVQB2 sweep) for 64 < n <= 128;
+// frags: gram_wide_fused_scratch_doubles() doubles of device scratch
+constexpr int kWideFusedMaxN = 128;
+size_t gram_wide_fused_scratch_doubles();
+cudaError_t launch_gram_wide_fused(const double* x, long long m, int n, long long ld, int op, const double* factor,
                                    int sm_count, double* frags, double* partial, double* c, StatusWord* status,
                                    cudaStream_t stream);
 

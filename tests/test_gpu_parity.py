@@ -147,10 +147,10 @@ def test_wide_gram(ctx, sq, oracle, m, n):
     cu = ctx.tsmttsm(big.t()[1:m + 1, :])
     ctx.synchronize()
     assert np.linalg.norm(cu.cpu().numpy() - c_ref) <= 5 * n * EPS * xn2
-    # the fused multiply keeps the n <= 64 limit, the fused solve stops at 128 columns, tsmttsm at 256
-    with pytest.raises(sq.ArgumentError):
-        ctx.tsmmttsmm(x, np.eye(n))
+    # the fused solve / multiply stop at 128 columns, tsmttsm at 256
     if n > 128:
+        with pytest.raises(sq.ArgumentError):
+            ctx.tsmmttsmm(x, np.eye(n))
         with pytest.raises(sq.ArgumentError):
             ctx.tsmRttsmR(x, np.eye(n))
     x[m // 2, n - 1] = np.inf
@@ -211,7 +211,50 @@ def test_wide_solve_gram_and_cholqr2(ctx, sq, oracle, m, n):
     assert np.array_equal(r_again, r)
 
 
+@pytest.mark.parametrize("m,n", [(4000, 65), (5003, 100), (9000, 128), (20011, 127), (300, 128)])
+def test_wide_multiply_gram_and_svqb2(ctx, sq, oracle, m, n):
+    """64 < n <= 128: tsmmttsmm (gram.cpp:142-151) and svqb2 (gram_qr.cpp:178-191; eigh_small's own
+    limit is 128 columns, gram_qr.cpp:62) through the fused multiply + Gram DMMA kernel."""
+    import torch
+    x = gaussian(m, n, seed=11 * n + m)
+    bm = np.asfortranarray(gaussian(n, n, seed=99) / np.sqrt(m))
+    c3_ref = oracle.port.tsmmttsmm(x, bm)
+    tol = 5 * n * EPS * np.linalg.norm(x @ bm) ** 2
+    c3 = ctx.tsmmttsmm(x, bm)
+    assert np.array_equal(c3, c3.T)
+    assert np.linalg.norm(c3 - c3_ref) <= tol
+    xd = torch.from_numpy(np.ascontiguousarray(x.T)).cuda().t()
+    bd = torch.from_numpy(np.ascontiguousarray(bm.T)).cuda().t()
+    c3d = ctx.tsmmttsmm(xd, bd)
+    ctx.synchronize()
+    assert np.linalg.norm(c3d.cpu().numpy() - c3_ref) <= tol
+    big = torch.zeros((n, m + 3), dtype=torch.float64, device="cuda")
+    big[:, 1:m + 1] = xd.t()
+    c3u = ctx.tsmmttsmm(big.t()[1:m + 1, :], bd)
+    ctx.synchronize()
+    assert np.linalg.norm(c3u.cpu().numpy() - c3_ref) <= tol
+    bad = bm.copy(order="F")
+    bad[n - 1, n - 2] = np.nan
+    with pytest.raises(sq.ArgumentError):
+        ctx.tsmmttsmm(x, bad)
+    # SVQB2
+    tr, z, sg, rank = ctx.svqb2(x)
+    tr_ref, z_ref, sg_ref, rank_ref = oracle.port.svqb2(x)
+    assert rank == rank_ref == n
+    assert np.linalg.norm(sg - sg_ref) <= 50 * n * EPS * sg_ref[0]
+    c = x.T @ x
+    assert np.linalg.norm(tr.T @ c @ tr - np.eye(n)) <= 1e-11
+    assert np.linalg.norm(z @ tr - np.eye(n)) <= 1e-11
+    assert np.linalg.norm(z.T @ z - c) <= 100 * n * EPS * np.linalg.norm(c)
+    trd, zd, sgd, rankd = ctx.svqb2(xd)
+    ctx.synchronize()
+    assert int(rankd) == n
+    assert np.linalg.norm(sgd.cpu().numpy() - sg_ref) <= 50 * n * EPS * sg_ref[0]
+
+
 def test_wide_gram_limit(ctx, sq):
+    with pytest.raises(sq.ArgumentError):
+        ctx.svqb2(gaussian(300, 129))
     with pytest.raises(sq.ArgumentError):
         ctx.cholqr2(gaussian(300, 129))
     with pytest.raises(sq.ArgumentError):

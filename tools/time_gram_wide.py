@@ -40,5 +40,16 @@ for n in (96, 128, 192, 256):
         ms2 = e0.elapsed_time(e1) / reps
         print(f"cholqr2 n={n:3d} m=2^{log2m} {ms2:8.3f} ms  {8.0*m*n/ms2/1e6:8.1f} GB/s effective  "
               f"second sweep {ms2-ms:8.3f} ms = executed DMMA {2.0*m*272*64/(ms2-ms)/1e9:6.2f} TF", flush=True)
+        for _ in range(2):
+            ctx.svqb2(x)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            ctx.svqb2(x)
+        e1.record()
+        torch.cuda.synchronize()
+        ctx.synchronize()
+        ms3 = e0.elapsed_time(e1) / reps
+        print(f"svqb2   n={n:3d} m=2^{log2m} {ms3:8.3f} ms  {8.0*m*n/ms3/1e6:8.1f} GB/s effective", flush=True)
     del x
     torch.cuda.empty_cache()
