@@ -646,7 +646,15 @@ int sqb_reconstruct_q_dev(sqb_context* ctx, const double* d_x, int64_t m, int64_
                           const double* d_r, double* d_q, int64_t ldq) {
   SQB_TRY(enter(ctx));
   if (n < 1 || m < 0) return SQB_E_DIMENSION;
-  if (n > 64 || ld < m || ldq < m) return SQB_E_ARGUMENT;
+  if (n > kWideFusedMaxN || ld < m || ldq < m) return SQB_E_ARGUMENT;
+  if (n > 64) {
+    SQB_TRY(grow(&ctx->work, &ctx->work_doubles, gram_wide_partial_doubles(static_cast<int>(n), ctx->sm_count) +
+                                                     gram_wide_fused_scratch_doubles()));
+    SQB_CUDA(launch_apply_rinv_wide(d_x, m, static_cast<int>(n), ld, d_r, ctx->sm_count, ctx->work, d_q, ldq,
+                                    ctx->d_status, ctx->stream));
+    ctx->launches += 2;
+    return SQB_OK;
+  }
   SQB_CUDA(launch_apply_rinv(d_x, m, static_cast<int>(n), ld, d_r, d_q, ldq, ctx->d_status,
                              ctx->stream));
   ctx->launches += 2;
@@ -865,7 +873,7 @@ int sqb_reconstruct_q_host(sqb_context* ctx, const double* x, int64_t m, int64_t
                            const double* r, double* q, int64_t ldq) {
   SQB_TRY(enter(ctx));
   if (n < 1 || m < 0) return SQB_E_DIMENSION;
-  if (n > 64 || ld < m || ldq < m) return SQB_E_ARGUMENT;
+  if (n > kWideFusedMaxN || ld < m || ldq < m) return SQB_E_ARGUMENT;
   const int nn = static_cast<int>(n);
   Small s;
   SQB_TRY(small_slots(ctx, nn, &s));

@@ -352,12 +352,12 @@ __global__ void __launch_bounds__(128, 1)
   }
 }
 
-// Q^T tiles of tile columns W and 15-W for the three row groups of a panel -> shared Q panel.
+// Q^T tiles of tile columns W and 15-W for the three row groups of a panel.  Lane (g,q) ends up with
+// Q[row 8t+2q+e, column 8J+g] in a?c[t][e].
 template <int W, int OP>
-__device__ __forceinline__ void solve_panel(const double* stage, const double* rf, double* qb, int lane,
-                                            int g, int q) {
-  constexpr int J1 = W, J2 = kWT - 1 - W, K1 = fused_k1(OP, W), K2 = fused_k2(OP, W), NT = kSolveP / 8;
-  double a1c[NT][2], a2c[NT][2];
+__device__ __forceinline__ void solve_tiles(const double* stage, const double* rf, double (&a1c)[kSolveP / 8][2],
+                                            double (&a2c)[kSolveP / 8][2], int lane, int g, int q) {
+  constexpr int K1 = fused_k1(OP, W), K2 = fused_k2(OP, W), NT = kSolveP / 8;
 #pragma unroll
   for (int t = 0; t < NT; ++t) a1c[t][0] = a1c[t][1] = a2c[t][0] = a2c[t][1] = 0.0;
   const double* rfw = rf + W * fused_ksteps(OP) * 32 + lane;
@@ -375,10 +375,40 @@ __device__ __forceinline__ void solve_panel(const double* stage, const double* r
       for (int t = 0; t < NT; ++t) dmma_w(a1c[t][0], a1c[t][1], a1, b[t]);
     }
   }
+}
+
+// ... to the shared Q panel in the SYRK's operand layout (one conflict-free 128-bit store per tile)
+template <int W, int OP>
+__device__ __forceinline__ void solve_panel(const double* stage, const double* rf, double* qb, int lane,
+                                            int g, int q) {
+  constexpr int J1 = W, J2 = kWT - 1 - W, NT = kSolveP / 8;
+  double a1c[NT][2], a2c[NT][2];
+  solve_tiles<W, OP>(stage, rf, a1c, a2c, lane, g, q);
 #pragma unroll
   for (int t = 0; t < NT; ++t) {
     *reinterpret_cast<double2*>(qb + (8 * J1 + g) * kSolveP + 8 * t + 2 * q) = make_double2(a1c[t][0], a1c[t][1]);
     *reinterpret_cast<double2*>(qb + (8 * J2 + g) * kSolveP + 8 * t + 2 * q) = make_double2(a2c[t][0], a2c[t][1]);
+  }
+}
+
+// ... or to global memory (reconstruct_q): a lane writes two consecutive rows of one column, the four
+// lanes of a column 64 contiguous bytes
+template <int W, int OP>
+__device__ __forceinline__ void solve_panel_out(const double* stage, const double* rf, double* qout, long long ldq,
+                                                long long r0, long long end, int n, int lane, int g, int q) {
+  constexpr int J1 = W, J2 = kWT - 1 - W, NT = kSolveP / 8;
+  double a1c[NT][2], a2c[NT][2];
+  solve_tiles<W, OP>(stage, rf, a1c, a2c, lane, g, q);
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    const long long row = r0 + 8 * t + 2 * q;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      if (row + e < end) {
+        if (8 * J1 + g < n) qout[row + e + static_cast<long long>(8 * J1 + g) * ldq] = a1c[t][e];
+        if (8 * J2 + g < n) qout[row + e + static_cast<long long>(8 * J2 + g) * ldq] = a2c[t][e];
+      }
+    }
   }
 }
 
@@ -388,9 +418,11 @@ struct WideSolveParams {
   int n, kb;
   const double* frags;  // U = R^-1 (rinv_wide_kernel) or B (bfrag_wide_kernel) in fragment order
   double* partial;      // one 128 x 128 column-major slab per CTA
+  double* qout;         // WRITEQ: Q = X U goes here (leading dimension ldq) and no Gram is formed
+  long long ldq;
 };
 
-template <int OP>
+template <int OP, bool WRITEQ>
 __global__ void __launch_bounds__(kWThreads, 1) gram_wide_fused_kernel(const WideSolveParams prm) {
   extern __shared__ __align__(128) double smem[];
   constexpr int kWStages = fused_stages(OP);  // shadows the plain kernel's ring depth
@@ -460,7 +492,7 @@ __global__ void __launch_bounds__(kWThreads, 1) gram_wide_fused_kernel(const Wid
     if (tid == 0 && nxt < npanels && will_be_async(nxt)) mbar_expect_tx(&bars[sn], tx_bytes);
     __syncthreads();  // GEMM(pn-1) done everywhere: stage sn free, Q panel (pn-1)&1 complete; SYRK(pn-2) done
     if (nxt < npanels) fill(nxt, sn);
-    if (pn > 0) {
+    if (!WRITEQ && pn > 0) {
       const double* qp = qbuf + ((pn - 1) & 1) * kStageDoubles;
 #define SQB_TRI(WV) tri_panel<WV, kSolveP>(qp, acc, g, q)
       SQB_WARP_SWITCH(SQB_TRI)
@@ -472,12 +504,19 @@ __global__ void __launch_bounds__(kWThreads, 1) gram_wide_fused_kernel(const Wid
         phase_bits ^= 1u << s;
       }
       const double* stage = smem + s * kStageDoubles;
-      double* qp = qbuf + (pn & 1) * kStageDoubles;
+      if (WRITEQ) {
+#define SQB_SOLVEQ(WV) solve_panel_out<WV, OP>(stage, rf, prm.qout, prm.ldq, begin + pn * kSolveP, end, prm.n, lane, g, q)
+        SQB_WARP_SWITCH(SQB_SOLVEQ)
+#undef SQB_SOLVEQ
+      } else {
+        double* qp = qbuf + (pn & 1) * kStageDoubles;
 #define SQB_SOLVE(WV) solve_panel<WV, OP>(stage, rf, qp, lane, g, q)
-      SQB_WARP_SWITCH(SQB_SOLVE)
+        SQB_WARP_SWITCH(SQB_SOLVE)
 #undef SQB_SOLVE
+      }
     }
   }
+  if (WRITEQ) return;
 
   double* dst = prm.partial + static_cast<long long>(blockIdx.x) * kWC * kWC;
 #define SQB_TRIS(WV) tri_store<WV>(dst, acc, g, q)
@@ -554,18 +593,47 @@ cudaError_t launch_gram_wide(const double* x, long long m, int n, long long ld, 
 
 size_t gram_wide_fused_scratch_doubles() { return fused_frag_doubles(OP_MULTIPLY); }
 
-template <int OP>
+template <int OP, bool WRITEQ = false>
 static cudaError_t launch_fused(const WideSolveParams& prm, cudaStream_t stream) {
   const size_t bytes = sizeof(double) * ((fused_stages(OP) + 2) * kWC * kSolveP + fused_frag_doubles(OP));
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gram_wide_fused_kernel<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(gram_wide_fused_kernel<OP, WRITEQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(bytes));
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  gram_wide_fused_kernel<OP><<<prm.kb, kWThreads, bytes, stream>>>(prm);
+  gram_wide_fused_kernel<OP, WRITEQ><<<prm.kb, kWThreads, bytes, stream>>>(prm);
   return cudaGetLastError();
+}
+
+static cudaError_t launch_rinv_wide(const double* r, int n, double* frags, StatusWord* status, cudaStream_t stream) {
+  static bool configured = false;
+  const size_t rinv_bytes = sizeof(double) * (tri_size(kWC) + kWC * kWC);
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(rinv_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(rinv_bytes));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  rinv_wide_kernel<<<1, 128, rinv_bytes, stream>>>(r, n, frags, status);
+  return cudaGetLastError();
+}
+
+static WideSolveParams fused_params(const double* x, long long m, int n, long long ld, const double* frags,
+                                    int sm_count) {
+  WideSolveParams prm;
+  prm.x = x;
+  prm.ld = ld;
+  prm.m = m;
+  prm.n = n;
+  prm.frags = frags;
+  prm.partial = nullptr;
+  prm.qout = nullptr;
+  prm.ldq = 0;
+  const long long panels = (m + kSolveP - 1) / kSolveP;
+  prm.kb = static_cast<int>(panels < sm_count ? (panels > 0 ? panels : 1) : sm_count);
+  return prm;
 }
 
 cudaError_t launch_gram_wide_fused(const double* x, long long m, int n, long long ld, int op, const double* factor,
@@ -574,33 +642,32 @@ cudaError_t launch_gram_wide_fused(const double* x, long long m, int n, long lon
   if (n <= 64 || n > kWideFusedMaxN || (op != OP_SOLVE && op != OP_MULTIPLY)) return cudaErrorInvalidValue;
   cudaError_t e;
   if (op == OP_SOLVE) {
-    static bool configured = false;
-    const size_t rinv_bytes = sizeof(double) * (tri_size(kWC) + kWC * kWC);
-    if (!configured) {
-      e = cudaFuncSetAttribute(rinv_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(rinv_bytes));
-      if (e != cudaSuccess) return e;
-      configured = true;
-    }
-    rinv_wide_kernel<<<1, 128, rinv_bytes, stream>>>(factor, n, frags, status);
+    e = launch_rinv_wide(factor, n, frags, status, stream);
   } else {
     bfrag_wide_kernel<<<16, 256, 0, stream>>>(factor, n, frags, status);
+    e = cudaGetLastError();
   }
-  e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  WideSolveParams prm;
-  prm.x = x;
-  prm.ld = ld;
-  prm.m = m;
-  prm.n = n;
-  prm.frags = frags;
+  WideSolveParams prm = fused_params(x, m, n, ld, frags, sm_count);
   prm.partial = partial;
-  const long long panels = (m + kSolveP - 1) / kSolveP;
-  prm.kb = static_cast<int>(panels < sm_count ? (panels > 0 ? panels : 1) : sm_count);
   e = op == OP_SOLVE ? launch_fused<OP_SOLVE>(prm, stream) : launch_fused<OP_MULTIPLY>(prm, stream);
   if (e != cudaSuccess) return e;
   gram_wide_reduce_kernel<<<(n * n + 255) / 256, 256, 0, stream>>>(partial, prm.kb, 0, n, c, 0, status);
   return cudaGetLastError();
+}
+
+// Q = X R^-1 for 64 < n <= 128 (reference reconstruct_q, src/gram_qr.cpp:193-221): the same solve GEMM,
+// tiles written straight to Q.
+cudaError_t launch_apply_rinv_wide(const double* x, long long m, int n, long long ld, const double* r,
+                                   int sm_count, double* frags, double* q, long long ldq, StatusWord* status,
+                                   cudaStream_t stream) {
+  if (n <= 64 || n > kWideFusedMaxN) return cudaErrorInvalidValue;
+  cudaError_t e = launch_rinv_wide(r, n, frags, status, stream);
+  if (e != cudaSuccess) return e;
+  WideSolveParams prm = fused_params(x, m, n, ld, frags, sm_count);
+  prm.qout = q;
+  prm.ldq = ldq;
+  return launch_fused<OP_SOLVE, true>(prm, stream);
 }
 
 }  // namespace sqb

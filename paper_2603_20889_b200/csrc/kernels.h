@@ -130,6 +130,10 @@ cudaError_t launch_gram_wide_fused(const double* x, long long m, int n, long lon
                                    int sm_count, double* frags, double* partial, double* c, StatusWord* status,
                                    cudaStream_t stream);
 
+cudaError_t launch_apply_rinv_wide(const double* x, long long m, int n, long long ld, const double* r,
+                                   int sm_count, double* frags, double* q, long long ldq, StatusWord* status,
+                                   cudaStream_t stream);
+
 // ---- gram_thread_kernels.cu (n <= 8: register-resident rows and accumulators) --------------
 constexpr int kThreadGramMaxN = 8;
 cudaError_t launch_gram_thread(const GramParams& prm, int op, long long num_blocks,

@@ -191,6 +191,14 @@ def test_wide_solve_gram_and_cholqr2(ctx, sq, oracle, m, n):
     xn = np.linalg.norm(x)
     r = ctx.cholqr2(x)
     r_ref = oracle.port.cholqr2(x)
+    # reconstruct_q (gram_qr.cpp:193-221) through the same solve GEMM
+    q = ctx.reconstruct_q(x, r)
+    q_ref = oracle.port.reconstruct_q(x, r_ref)
+    assert np.linalg.norm(q - q_ref) <= 1e-11 * np.sqrt(n)
+    assert np.linalg.norm(q.T @ q - np.eye(n)) <= 1e-12
+    qd = ctx.reconstruct_q(xd, torch.from_numpy(np.ascontiguousarray(r.T)).cuda().t())
+    ctx.synchronize()
+    assert np.array_equal(qd.cpu().numpy(), q)
     assert np.all(np.tril(r, -1) == 0.0) and np.all(np.diag(r) > 0.0)
     assert np.linalg.norm(r - r_ref) <= 64 * n * EPS * xn
     assert np.linalg.norm(r.T @ r - c_ref) <= 50 * n * EPS * xn ** 2
