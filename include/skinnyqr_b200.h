@@ -93,10 +93,12 @@ int sqb_block_qless_qr_dev(sqb_context* ctx, const double* d_x, int64_t m, int64
  * the wide FP64 tensor-core kernel and ignore num_blocks / panel_rows (BASELINE config 5)   */
 int sqb_tsmttsm_dev(sqb_context* ctx, const double* d_x, int64_t m, int64_t n, int64_t ld,
                     int64_t num_blocks, int64_t panel_rows, double* d_c);
-/* C = (X R^-1)^T (X R^-1), R upper triangular n x n on device (tsmRttsmR); n <= 64        */
+/* C = (X R^-1)^T (X R^-1), R upper triangular n x n on device (tsmRttsmR); n <= 128: the
+ * reference has no column limit; 65..128 columns run the wide fused kernel (explicit R^-1 as a
+ * tensor-core GEMM feeding the SYRK) and ignore num_blocks / panel_rows                       */
 int sqb_tsmRttsmR_dev(sqb_context* ctx, const double* d_x, int64_t m, int64_t n, int64_t ld,
                       const double* d_r, int64_t num_blocks, int64_t panel_rows, double* d_c);
-/* C = (X B)^T (X B), B dense n x n on device                 (tsmmttsmm); n <= 64          */
+/* C = (X B)^T (X B), B dense n x n on device (tsmmttsmm); n <= 128, as above               */
 int sqb_tsmmttsmm_dev(sqb_context* ctx, const double* d_x, int64_t m, int64_t n, int64_t ld,
                       const double* d_b, int64_t num_blocks, int64_t panel_rows, double* d_c);
 
@@ -106,17 +108,19 @@ int sqb_eigh_small_dev(sqb_context* ctx, const double* d_c, int64_t n, double* d
                        double* d_vectors);
 
 /* ---- Gram-based drivers (gram_qr.hpp:46-59, src/gram_qr.cpp:123-221) ----------------------- */
-/* cholqr2: two streaming passes, both Cholesky factorisations and R2*R1 stay on the device.  */
+/* cholqr2: two streaming passes, both Cholesky factorisations and R2*R1 stay on the device.
+ * n <= 128 (the reference has no column limit; 65..128 columns take the wide kernels).       */
 int sqb_cholqr2_dev(sqb_context* ctx, const double* d_x, int64_t m, int64_t n, int64_t ld,
                     int64_t num_blocks, int64_t panel_rows, double* d_r);
-/* svqb2: d_transform (B), d_z are n x n, d_sigma has n entries, d_rank one int64.           */
+/* svqb2: d_transform (B), d_z are n x n, d_sigma has n entries, d_rank one int64.
+ * n <= 128 = the reference's own limit (eigh_small, gram_qr.cpp:62).                         */
 int sqb_svqb2_dev(sqb_context* ctx, const double* d_x, int64_t m, int64_t n, int64_t ld,
                   int64_t num_blocks, int64_t panel_rows, double* d_transform, double* d_z,
                   double* d_sigma, int64_t* d_rank);
 /* One SVQB pass on a device Gram matrix (svqb_pass, gram_qr.cpp:133-176).                    */
 int sqb_svqb_pass_dev(sqb_context* ctx, const double* d_c, int64_t n, double* d_b, double* d_z,
                       double* d_sigma, int64_t* d_rank);
-/* Q = X R^-1 written to d_q (ldq) (reconstruct_q, gram_qr.cpp:193-221).                      */
+/* Q = X R^-1 written to d_q (ldq) (reconstruct_q, gram_qr.cpp:193-221); n <= 128.           */
 int sqb_reconstruct_q_dev(sqb_context* ctx, const double* d_x, int64_t m, int64_t n, int64_t ld,
                           const double* d_r, double* d_q, int64_t ldq);
 

@@ -54,11 +54,11 @@ __device__ __forceinline__ double2 frag(const double* stage, int tile, int t, in
 }
 
 // Triangular chunk, warp W: tile rows W and 15-W of the 16 x 16 upper block triangle.
-template <int W, int PP = kTriP>
+template <int W, int PP = kTriP, int ROWS = PP>
 __device__ __forceinline__ void tri_panel(const double* stage, double (&acc)[32][2], int g, int q) {
   constexpr int R1 = W, R2 = kWT - 1 - W;
 #pragma unroll
-  for (int t = 0; t < PP / 8; ++t) {
+  for (int t = 0; t < ROWS / 8; ++t) {
     double2 b[kWT - R1];
 #pragma unroll
     for (int j = R1; j < kWT; ++j) b[j - R1] = frag<PP>(stage, j, t, g, q);
@@ -255,7 +255,12 @@ __global__ void __launch_bounds__(kWThreads, 1) gram_wide_kernel(const WideParam
 // panel.  Same forward error class as the substitution (|dQ| <~ n eps |X| |R^-1|); deviation noted
 // in DESIGN.md.
 // ------------------------------------------------------------------------------------------------
-constexpr int kSolveP = 24;       // panel rows == pitch == 8 (mod 16)
+// Panel geometry per variant.  The solve GEMM reads the X stage with the transposed LDS.64 pattern
+// ((4k+q) * pitch + 8t + g): conflict-free for pitch = 4 or 12 (mod 16); the SYRK reads the Q panel with
+// the LDS.128 pattern ((8T+g) * pitch + 8t + 2q): conflict-free for pitch = 8 (mod 16).
+__host__ __device__ constexpr int fused_rows(int op) { return op == OP_SOLVE ? 24 : 16; }
+__host__ __device__ constexpr int fused_spitch(int op) { return op == OP_SOLVE ? 28 : 20; }
+constexpr int kQPitch = 24;
 // k4 steps per warp: triangular factor (OP_SOLVE, U = R^-1) (2w+2) + (32-2w) = 34; dense factor
 // (OP_MULTIPLY, B) 32 + 32
 __host__ __device__ constexpr int fused_ksteps(int op) { return op == OP_SOLVE ? 34 : 64; }
@@ -264,7 +269,10 @@ __host__ __device__ constexpr int fused_k2(int op, int w) { return op == OP_SOLV
 __host__ __device__ constexpr int fused_frag_doubles(int op) { return 8 * fused_ksteps(op) * 32; }
 // panels in flight: the fused passes are far on the tensor-pipe side (a panel is ~5 us of DMMAs), so the
 // dense factor's 128 KB of fragments may squeeze the ring down to two stages
-__host__ __device__ constexpr int fused_stages(int op) { return op == OP_SOLVE ? 4 : 2; }
+__host__ __device__ constexpr int fused_stages(int op) { return op == OP_SOLVE ? 3 : 2; }
+__host__ __device__ constexpr size_t fused_smem_doubles(int op) {
+  return static_cast<size_t>(fused_stages(op)) * kWC * fused_spitch(op) + 2 * kWC * kQPitch + fused_frag_doubles(op);
+}
 constexpr double kEpsW = 2.220446049250313e-16;
 
 // Factor element held by lane (g,q) of warp w at issue step f: tile column w for the first k1 steps,
@@ -352,61 +360,77 @@ __global__ void __launch_bounds__(128, 1)
   }
 }
 
-// Q^T tiles of tile columns W and 15-W for the three row groups of a panel.  Lane (g,q) ends up with
-// Q[row 8t+2q+e, column 8J+g] in a?c[t][e].
-template <int W, int OP>
-__device__ __forceinline__ void solve_tiles(const double* stage, const double* rf, double (&a1c)[kSolveP / 8][2],
-                                            double (&a2c)[kSolveP / 8][2], int lane, int g, int q) {
-  constexpr int K1 = fused_k1(OP, W), K2 = fused_k2(OP, W), NT = kSolveP / 8;
+// Q^T tiles of tile columns w and 15-w for the row groups of a panel.  Lane (g,q) ends up with
+// Q[row 8t+2q+e, column 8J+g] in a?c[t][e].  One loop with run-time bounds for all warps (the warp index
+// only sets the trip counts), so the GEMM half of the kernel is not replicated eight times in the
+// instruction cache like the register-indexed SYRK has to be.
+template <int OP>
+__device__ __forceinline__ void solve_tiles(const double* stage, const double* rf, double (&a1c)[fused_rows(OP) / 8][2],
+                                            double (&a2c)[fused_rows(OP) / 8][2], int w, int kmax, int lane, int g,
+                                            int q) {
+  constexpr int NT = fused_rows(OP) / 8, SP = fused_spitch(OP);
+  // kmax = ceil(n / 4): columns of X beyond n are zero, so are the factor rows beyond n
+  const int k1 = min(fused_k1(OP, w), kmax), k2 = min(fused_k2(OP, w), kmax);
 #pragma unroll
   for (int t = 0; t < NT; ++t) a1c[t][0] = a1c[t][1] = a2c[t][0] = a2c[t][1] = 0.0;
-  const double* rfw = rf + W * fused_ksteps(OP) * 32 + lane;
-#pragma unroll
-  for (int kk = 0; kk < K2; ++kk) {
+  const double* rf1 = rf + w * fused_ksteps(OP) * 32 + lane;
+  const double* rf2 = rf1 + fused_k1(OP, w) * 32;
+  const double* sb = stage + q * SP + g;
+  int kk = 0;
+#pragma unroll 2
+  for (; kk < k1; ++kk) {  // both tile columns (k1 <= k2)
     double b[NT];
 #pragma unroll
-    for (int t = 0; t < NT; ++t) b[t] = stage[(4 * kk + q) * kSolveP + 8 * t + g];
-    const double a2 = rfw[(K1 + kk) * 32];
+    for (int t = 0; t < NT; ++t) b[t] = sb[4 * kk * SP + 8 * t];
+    const double a2 = rf2[kk * 32], a1 = rf1[kk * 32];
 #pragma unroll
     for (int t = 0; t < NT; ++t) dmma_w(a2c[t][0], a2c[t][1], a2, b[t]);
-    if (kk < K1) {
-      const double a1 = rfw[kk * 32];
 #pragma unroll
-      for (int t = 0; t < NT; ++t) dmma_w(a1c[t][0], a1c[t][1], a1, b[t]);
-    }
+    for (int t = 0; t < NT; ++t) dmma_w(a1c[t][0], a1c[t][1], a1, b[t]);
+  }
+#pragma unroll 2
+  for (; kk < k2; ++kk) {  // the longer column only (triangular factor)
+    double b[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) b[t] = sb[4 * kk * SP + 8 * t];
+    const double a2 = rf2[kk * 32];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) dmma_w(a2c[t][0], a2c[t][1], a2, b[t]);
   }
 }
 
 // ... to the shared Q panel in the SYRK's operand layout (one conflict-free 128-bit store per tile)
-template <int W, int OP>
-__device__ __forceinline__ void solve_panel(const double* stage, const double* rf, double* qb, int lane,
-                                            int g, int q) {
-  constexpr int J1 = W, J2 = kWT - 1 - W, NT = kSolveP / 8;
+template <int OP>
+__device__ __forceinline__ void solve_panel(const double* stage, const double* rf, double* qb, int n, int w,
+                                            int lane, int g, int q) {
+  constexpr int NT = fused_rows(OP) / 8;
+  const int j1 = w, j2 = kWT - 1 - w;
   double a1c[NT][2], a2c[NT][2];
-  solve_tiles<W, OP>(stage, rf, a1c, a2c, lane, g, q);
+  solve_tiles<OP>(stage, rf, a1c, a2c, w, (n + 3) / 4, lane, g, q);
 #pragma unroll
   for (int t = 0; t < NT; ++t) {
-    *reinterpret_cast<double2*>(qb + (8 * J1 + g) * kSolveP + 8 * t + 2 * q) = make_double2(a1c[t][0], a1c[t][1]);
-    *reinterpret_cast<double2*>(qb + (8 * J2 + g) * kSolveP + 8 * t + 2 * q) = make_double2(a2c[t][0], a2c[t][1]);
+    *reinterpret_cast<double2*>(qb + (8 * j1 + g) * kQPitch + 8 * t + 2 * q) = make_double2(a1c[t][0], a1c[t][1]);
+    *reinterpret_cast<double2*>(qb + (8 * j2 + g) * kQPitch + 8 * t + 2 * q) = make_double2(a2c[t][0], a2c[t][1]);
   }
 }
 
 // ... or to global memory (reconstruct_q): a lane writes two consecutive rows of one column, the four
 // lanes of a column 64 contiguous bytes
-template <int W, int OP>
+template <int OP>
 __device__ __forceinline__ void solve_panel_out(const double* stage, const double* rf, double* qout, long long ldq,
-                                                long long r0, long long end, int n, int lane, int g, int q) {
-  constexpr int J1 = W, J2 = kWT - 1 - W, NT = kSolveP / 8;
+                                                long long r0, long long end, int n, int w, int lane, int g, int q) {
+  constexpr int NT = fused_rows(OP) / 8;
+  const int j1 = w, j2 = kWT - 1 - w;
   double a1c[NT][2], a2c[NT][2];
-  solve_tiles<W, OP>(stage, rf, a1c, a2c, lane, g, q);
+  solve_tiles<OP>(stage, rf, a1c, a2c, w, (n + 3) / 4, lane, g, q);
 #pragma unroll
   for (int t = 0; t < NT; ++t) {
     const long long row = r0 + 8 * t + 2 * q;
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       if (row + e < end) {
-        if (8 * J1 + g < n) qout[row + e + static_cast<long long>(8 * J1 + g) * ldq] = a1c[t][e];
-        if (8 * J2 + g < n) qout[row + e + static_cast<long long>(8 * J2 + g) * ldq] = a2c[t][e];
+        if (8 * j1 + g < n) qout[row + e + static_cast<long long>(8 * j1 + g) * ldq] = a1c[t][e];
+        if (8 * j2 + g < n) qout[row + e + static_cast<long long>(8 * j2 + g) * ldq] = a2c[t][e];
       }
     }
   }
@@ -425,11 +449,11 @@ struct WideSolveParams {
 template <int OP, bool WRITEQ>
 __global__ void __launch_bounds__(kWThreads, 1) gram_wide_fused_kernel(const WideSolveParams prm) {
   extern __shared__ __align__(128) double smem[];
-  constexpr int kWStages = fused_stages(OP);  // shadows the plain kernel's ring depth
-  __shared__ uint64_t bars[kWStages];
-  constexpr int kStageDoubles = kWC * kSolveP;
-  double* qbuf = smem + kWStages * kStageDoubles;  // two Q panels
-  double* rf = qbuf + 2 * kStageDoubles;           // U fragments
+  constexpr int NSTAGE = fused_stages(OP), P = fused_rows(OP), SP = fused_spitch(OP);
+  __shared__ uint64_t bars[NSTAGE];
+  constexpr int kStageDoubles = kWC * SP, kQDoubles = kWC * kQPitch;
+  double* qbuf = smem + NSTAGE * kStageDoubles;  // two Q panels
+  double* rf = qbuf + 2 * kQDoubles;             // factor fragments
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
   const int rb = blockIdx.x;
@@ -438,17 +462,17 @@ __global__ void __launch_bounds__(kWThreads, 1) gram_wide_fused_kernel(const Wid
   const bool slot_ok = slot < kWC && slot < prm.n;
   const int valid_slots = prm.n < kWC ? prm.n : kWC;
 
-  for (int i = tid; i < (kWStages + 2) * kStageDoubles; i += kWThreads) smem[i] = 0.0;
+  for (int i = tid; i < NSTAGE * kStageDoubles + 2 * kQDoubles; i += kWThreads) smem[i] = 0.0;
   for (int i = tid; i < fused_frag_doubles(OP); i += kWThreads) rf[i] = prm.frags[i];
-  if (tid < kWStages) mbar_init(&bars[tid], 1);
+  if (tid < NSTAGE) mbar_init(&bars[tid], 1);
   mbar_fence_init();
   __syncthreads();
 
   long long rpb = (prm.m + prm.kb - 1) / prm.kb;
-  rpb = (rpb + kSolveP - 1) / kSolveP * kSolveP;
+  rpb = (rpb + P - 1) / P * P;
   const long long begin = min(static_cast<long long>(rb) * rpb, prm.m);
   const long long end = min(static_cast<long long>(rb + 1) * rpb, prm.m);
-  const long long npanels = (end - begin + kSolveP - 1) / kSolveP;
+  const long long npanels = (end - begin + P - 1) / P;
   const bool aligned = ((reinterpret_cast<uintptr_t>(prm.x) & 15) == 0) && ((prm.ld & 1) == 0);
   const double* colp = prm.x + static_cast<long long>(slot_ok ? slot : 0) * prm.ld;
 
@@ -457,44 +481,44 @@ __global__ void __launch_bounds__(kWThreads, 1) gram_wide_fused_kernel(const Wid
   for (int p = 0; p < 32; ++p) acc[p][0] = acc[p][1] = 0.0;
 
   uint32_t phase_bits = 0, async_bits = 0;
-  auto will_be_async = [&](long long pn) { return aligned && begin + pn * kSolveP + kSolveP <= end; };
+  auto will_be_async = [&](long long pn) { return aligned && begin + pn * P + P <= end; };
   auto fill = [&](long long pn, int s) {
-    const long long r0 = begin + pn * kSolveP;
+    const long long r0 = begin + pn * P;
     double* st = smem + s * kStageDoubles;
     if (will_be_async(pn)) {
       if (slot_ok) {
         fence_async_smem();
-        bulk_g2s(st + slot * kSolveP, colp + r0, kSolveP * sizeof(double), &bars[s]);
+        bulk_g2s(st + slot * SP, colp + r0, P * sizeof(double), &bars[s]);
       }
       async_bits |= 1u << s;
     } else {
       if (slot_ok) {
-        for (int r = 0; r < kSolveP; ++r) st[slot * kSolveP + r] = (r0 + r < end) ? __ldg(colp + r0 + r) : 0.0;
+        for (int r = 0; r < P; ++r) st[slot * SP + r] = (r0 + r < end) ? __ldg(colp + r0 + r) : 0.0;
       }
       async_bits &= ~(1u << s);
     }
   };
-  const uint32_t tx_bytes = static_cast<uint32_t>(valid_slots * kSolveP * sizeof(double));
+  const uint32_t tx_bytes = static_cast<uint32_t>(valid_slots * P * sizeof(double));
 
   if (tid == 0) {
-    for (int s = 0; s < kWStages - 1; ++s)
+    for (int s = 0; s < NSTAGE - 1; ++s)
       if (s < npanels && will_be_async(s)) mbar_expect_tx(&bars[s], tx_bytes);
   }
   __syncthreads();
-  for (int s = 0; s < kWStages - 1; ++s)
+  for (int s = 0; s < NSTAGE - 1; ++s)
     if (s < npanels) fill(s, s);
 
   // iteration pn: SYRK of panel pn-1 (from its Q panel), then the solve GEMM of panel pn
   for (long long pn = 0; pn <= npanels; ++pn) {
-    const int s = static_cast<int>(pn % kWStages);
-    const long long nxt = pn + kWStages - 1;
-    const int sn = static_cast<int>(nxt % kWStages);
+    const int s = static_cast<int>(pn % NSTAGE);
+    const long long nxt = pn + NSTAGE - 1;
+    const int sn = static_cast<int>(nxt % NSTAGE);
     if (tid == 0 && nxt < npanels && will_be_async(nxt)) mbar_expect_tx(&bars[sn], tx_bytes);
     __syncthreads();  // GEMM(pn-1) done everywhere: stage sn free, Q panel (pn-1)&1 complete; SYRK(pn-2) done
     if (nxt < npanels) fill(nxt, sn);
     if (!WRITEQ && pn > 0) {
-      const double* qp = qbuf + ((pn - 1) & 1) * kStageDoubles;
-#define SQB_TRI(WV) tri_panel<WV, kSolveP>(qp, acc, g, q)
+      const double* qp = qbuf + ((pn - 1) & 1) * kQDoubles;
+#define SQB_TRI(WV) tri_panel<WV, kQPitch, P>(qp, acc, g, q)
       SQB_WARP_SWITCH(SQB_TRI)
 #undef SQB_TRI
     }
@@ -504,16 +528,8 @@ __global__ void __launch_bounds__(kWThreads, 1) gram_wide_fused_kernel(const Wid
         phase_bits ^= 1u << s;
       }
       const double* stage = smem + s * kStageDoubles;
-      if (WRITEQ) {
-#define SQB_SOLVEQ(WV) solve_panel_out<WV, OP>(stage, rf, prm.qout, prm.ldq, begin + pn * kSolveP, end, prm.n, lane, g, q)
-        SQB_WARP_SWITCH(SQB_SOLVEQ)
-#undef SQB_SOLVEQ
-      } else {
-        double* qp = qbuf + (pn & 1) * kStageDoubles;
-#define SQB_SOLVE(WV) solve_panel<WV, OP>(stage, rf, qp, lane, g, q)
-        SQB_WARP_SWITCH(SQB_SOLVE)
-#undef SQB_SOLVE
-      }
+      if (WRITEQ) solve_panel_out<OP>(stage, rf, prm.qout, prm.ldq, begin + pn * P, end, prm.n, warp, lane, g, q);
+      else solve_panel<OP>(stage, rf, qbuf + (pn & 1) * kQDoubles, prm.n, warp, lane, g, q);
     }
   }
   if (WRITEQ) return;
@@ -595,7 +611,7 @@ size_t gram_wide_fused_scratch_doubles() { return fused_frag_doubles(OP_MULTIPLY
 
 template <int OP, bool WRITEQ = false>
 static cudaError_t launch_fused(const WideSolveParams& prm, cudaStream_t stream) {
-  const size_t bytes = sizeof(double) * ((fused_stages(OP) + 2) * kWC * kSolveP + fused_frag_doubles(OP));
+  const size_t bytes = sizeof(double) * fused_smem_doubles(OP);
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(gram_wide_fused_kernel<OP, WRITEQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -621,7 +637,7 @@ static cudaError_t launch_rinv_wide(const double* r, int n, double* frags, Statu
 }
 
 static WideSolveParams fused_params(const double* x, long long m, int n, long long ld, const double* frags,
-                                    int sm_count) {
+                                    int sm_count, int op) {
   WideSolveParams prm;
   prm.x = x;
   prm.ld = ld;
@@ -631,7 +647,7 @@ static WideSolveParams fused_params(const double* x, long long m, int n, long lo
   prm.partial = nullptr;
   prm.qout = nullptr;
   prm.ldq = 0;
-  const long long panels = (m + kSolveP - 1) / kSolveP;
+  const long long panels = (m + fused_rows(op) - 1) / fused_rows(op);
   prm.kb = static_cast<int>(panels < sm_count ? (panels > 0 ? panels : 1) : sm_count);
   return prm;
 }
@@ -648,7 +664,7 @@ cudaError_t launch_gram_wide_fused(const double* x, long long m, int n, long lon
     e = cudaGetLastError();
   }
   if (e != cudaSuccess) return e;
-  WideSolveParams prm = fused_params(x, m, n, ld, frags, sm_count);
+  WideSolveParams prm = fused_params(x, m, n, ld, frags, sm_count, op);
   prm.partial = partial;
   e = op == OP_SOLVE ? launch_fused<OP_SOLVE>(prm, stream) : launch_fused<OP_MULTIPLY>(prm, stream);
   if (e != cudaSuccess) return e;
@@ -664,7 +680,7 @@ cudaError_t launch_apply_rinv_wide(const double* x, long long m, int n, long lon
   if (n <= 64 || n > kWideFusedMaxN) return cudaErrorInvalidValue;
   cudaError_t e = launch_rinv_wide(r, n, frags, status, stream);
   if (e != cudaSuccess) return e;
-  WideSolveParams prm = fused_params(x, m, n, ld, frags, sm_count);
+  WideSolveParams prm = fused_params(x, m, n, ld, frags, sm_count, OP_SOLVE);
   prm.qout = q;
   prm.ldq = ldq;
   return launch_fused<OP_SOLVE, true>(prm, stream);

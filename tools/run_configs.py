@@ -168,6 +168,7 @@ torch.cuda.empty_cache()
 
 # ---- C5 ----------------------------------------------------------------------------------------
 # transitional regime: the Gram matrix of a 2^24 x n matrix, n = 128 / 256, on the FP64 tensor cores.
+# CholQR2 and SVQB2 run up to 128 columns (fused solve / multiply + Gram on the tensor cores).
 # The reference's tsqr_qless rejects n > 64 (tsqr.cpp:188), so there is no TSQR arm at these widths;
 # the widest TSQR (n = 64) is timed beside it for the flop-rate comparison.
 m = (1 << 20) if small else (1 << 24)
@@ -190,6 +191,16 @@ for n in (64, 128, 256):
     c_ref = ref.tsmttsm(xh)
     row["parity_err_F_at_2^17_rows"] = float(np.linalg.norm(c_gpu.cpu().numpy() - c_ref))
     row["parity_bound_5_n_eps_normX2"] = float(5 * n * EPS * np.linalg.norm(xh) ** 2)
+    if n <= 128:  # CholQR2 / SVQB2 through the fused wide sweeps (n <= 128), parity against the reference
+        row["cholqr2_ms"] = gpu_ms(lambda: ctx.cholqr2(x), 3, 1)
+        row["cholqr2_gbs_effective"] = 8.0 * m * n / row["cholqr2_ms"] / 1e6
+        row["svqb2_ms"] = gpu_ms(lambda: ctx.svqb2(x), 3, 1)
+        row["svqb2_gbs_effective"] = 8.0 * m * n / row["svqb2_ms"] / 1e6
+        r_gpu = ctx.cholqr2(x[:mc])
+        ctx.synchronize()
+        r_ref = ref.cholqr2(xh)
+        row["cholqr2_parity_err_F_at_2^17_rows"] = float(np.linalg.norm(r_gpu.cpu().numpy() - r_ref))
+        row["cholqr2_parity_bound_64_n_eps_normX"] = float(64 * n * EPS * np.linalg.norm(xh))
     if n <= 64:
         row["tsqr_ms"] = gpu_ms(lambda: ctx.tsqr_qless(x), 3, 1)
         row["tsqr_tflops_2mn2"] = 2.0 * m * n * n / row["tsqr_ms"] / 1e9
