@@ -113,15 +113,18 @@ def test_device_stream_and_cli_end_to_end(tmp_path, oracle):
     assert out.returncode == 0, out.stderr
     r = tio.matrix_read(tmp_path / "r.tskm")
     assert np.linalg.norm(r - oracle.port.tsqr_qless(a)) <= 64 * n * np.finfo(float).eps * np.linalg.norm(a)
-    out = run_cli("bench", "--mn-product", str(1 << 20), "--cols", "1,8,65", "--methods", "tsqr,cholqr2,svqb2",
+    out = run_cli("bench", "--mn-product", str(1 << 20), "--cols", "1,8,65,129", "--methods", "tsqr,cholqr2,svqb2",
                   "--reps", "5", "--format", "json")
     assert out.returncode == 0, out.stderr
     rows = json.loads(out.stdout)
-    assert len(rows) == 9
-    good = [r for r in rows if r["n"] != 65]
+    assert len(rows) == 12
+    # TSQR stops at 64 columns (tsqr.cpp:188), the Gram-based methods at 128 here
+    good = [r for r in rows if r["n"] <= 8 or (r["n"] == 65 and r["method"] != "tsqr")]
+    assert len(good) == 8
     assert all(isinstance(r["orth_resid"], float) and r["orth_resid"] <= 1e-12 and r["model_ratio"] > 0 for r in good)
     assert all(r["large_reads"] == (1 if r["method"] == "tsqr" else 2) * r["m"] * r["n"] for r in good)
-    assert all(r["orth_resid"] == "ArgumentError" for r in rows if r["n"] == 65)  # per-row error, the grid continues
+    bad = [r for r in rows if r not in good]
+    assert len(bad) == 4 and all(r["orth_resid"] == "ArgumentError" for r in bad)  # per-row error, the grid continues
     assert run_cli("bench", "--reps", "0").returncode != 0
 
 

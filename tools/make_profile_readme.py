@@ -161,6 +161,18 @@ if cf.exists():
         for r in c["C5"]:
             ts = f"{r['tsqr_ms']:.1f} ms = {r['tsqr_tflops_2mn2']:.1f} TFLOP/s" if "tsqr_ms" in r else "reference rejects n > 64"
             out.append(f"| {r['n']} | {r['tsmttsm_ms']:.2f} | {r['gbs']:.0f} | {r['nominal_tflops_2mn2']:.1f} | {r['executed_dmma_tflops']:.1f} | {100*r['dmma_pipe_util_vs_37.1']:.0f} % | {r['parity_err_F_at_2^17_rows']:.1e} ({r['parity_bound_5_n_eps_normX2']:.1e}) | {ts} |")
+        if any("cholqr2_ms" in r for r in c["C5"]):
+            out.append("\nCholQR2 / SVQB2 at the same sizes (n <= 128: fused solve / multiply + Gram sweeps on the tensor cores; effective GB/s = 8mn / t):\n")
+            out.append("| n | CholQR2 ms | GB/s | R parity err at 2^17 rows (bound 64 n eps |X|) | SVQB2 ms | GB/s |")
+            out.append("|---|---|---|---|---|---|")
+            for r in c["C5"]:
+                if "cholqr2_ms" in r:
+                    out.append(f"| {r['n']} | {r['cholqr2_ms']:.2f} | {r['cholqr2_gbs_effective']:.0f} | {r['cholqr2_parity_err_F_at_2^17_rows']:.1e} ({r['cholqr2_parity_bound_64_n_eps_normX']:.1e}) | {r['svqb2_ms']:.2f} | {r['svqb2_gbs_effective']:.0f} |")
+
+wide = G / f"{tag}_wide.txt"
+if wide.exists():
+    shutil.copy(wide, P / f"{tag}_wide.txt")
+    out.append(f"\n## Wide column counts at m = 2^24 ({tag}_wide.txt; `tools/time_gram_wide.py`)\n\n```\n{wide.read_text().strip()}\n```")
 
 clk = G / f"{tag}_clocks.csv"
 if clk.exists():
