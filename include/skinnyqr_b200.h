@@ -127,7 +127,8 @@ int sqb_reconstruct_q_dev(sqb_context* ctx, const double* d_x, int64_t m, int64_
 /* ---- least squares (include/skinnyqr/lstsq.hpp:21, src/lstsq.cpp:13-61) -------------------- */
 /* A (m x n, lda) and rhs (m) stay separate device arrays: column n of the [A rhs] pencil is
  * read straight from d_rhs, so the reference's m*(n+1) assembly copy (lstsq.cpp:24-26) never
- * happens.  d_xsol gets n entries, d_residual one.                                          */
+ * happens.  d_xsol gets n entries, d_residual one.  n + 1 <= 64 on the TSQR route (tsqr.cpp:188),
+ * n + 1 <= 128 on the CholQR2 / SVQB2 routes.                                                 */
 int sqb_solve_lstsq_dev(sqb_context* ctx, const double* d_a, int64_t m, int64_t n, int64_t lda,
                         const double* d_rhs, int method, double* d_xsol, double* d_residual);
 

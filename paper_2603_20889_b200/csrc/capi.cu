@@ -203,20 +203,20 @@ int cholqr2_view(sqb_context* ctx, const MatView& v, long long m, int n, long lo
 }
 
 // ---- wide column counts (64 < n): plain Gram up to 256 columns, fused solve + Gram up to 128 ----
-int gram_wide_view(sqb_context* ctx, const double* d_x, long long m, int n, long long ld, int op,
-                   const double* factor, double* d_c, bool check) {
+int gram_wide_view(sqb_context* ctx, const MatView& v, long long m, int n, int op, const double* factor,
+                   double* d_c, bool check) {
   const size_t partial = gram_wide_partial_doubles(n, ctx->sm_count);
   if (op == OP_PLAIN) {
     if (n > kWideGramMaxN) return SQB_E_ARGUMENT;
     SQB_TRY(grow(&ctx->work, &ctx->work_doubles, partial + gram_wide_fused_scratch_doubles()));
-    SQB_CUDA(launch_gram_wide(d_x, m, n, ld, ctx->sm_count, ctx->work, d_c, check ? 1 : 0, ctx->d_status,
+    SQB_CUDA(launch_gram_wide(v, m, n, ctx->sm_count, ctx->work, d_c, check ? 1 : 0, ctx->d_status,
                               ctx->stream));
     ctx->launches += 2;
     return SQB_OK;
   }
   if (n > kWideFusedMaxN) return SQB_E_ARGUMENT;
   SQB_TRY(grow(&ctx->work, &ctx->work_doubles, partial + gram_wide_fused_scratch_doubles()));
-  SQB_CUDA(launch_gram_wide_fused(d_x, m, n, ld, op, factor, ctx->sm_count, ctx->work + partial, ctx->work, d_c,
+  SQB_CUDA(launch_gram_wide_fused(v, m, n, op, factor, ctx->sm_count, ctx->work + partial, ctx->work, d_c,
                                   ctx->d_status, ctx->stream));
   ctx->launches += 3;
   return SQB_OK;
@@ -224,14 +224,14 @@ int gram_wide_view(sqb_context* ctx, const double* d_x, long long m, int n, long
 
 // CholQR2 beyond 64 columns (the reference's cholqr2 has no column limit, gram_qr.cpp:123-131): the
 // wide SYRK, the one-CTA Cholesky (n <= 128), the fused solve + Gram sweep, Cholesky, R = R2 R1.
-int cholqr2_wide(sqb_context* ctx, const double* d_x, long long m, int n, long long ld, double* d_r,
+int cholqr2_wide(sqb_context* ctx, const MatView& v, long long m, int n, double* d_r,
                  const std::function<int(double*)>& allreduce) {
   Small s;
   SQB_TRY(small_slots(ctx, n, &s));
-  SQB_TRY(gram_wide_view(ctx, d_x, m, n, ld, OP_PLAIN, nullptr, s.c1, true));
+  SQB_TRY(gram_wide_view(ctx, v, m, n, OP_PLAIN, nullptr, s.c1, true));
   if (allreduce) SQB_TRY(allreduce(s.c1));
   SQB_CUDA(launch_cholesky(s.c1, n, s.r1, ctx->d_status, ctx->stream));
-  SQB_TRY(gram_wide_view(ctx, d_x, m, n, ld, OP_SOLVE, s.r1, s.c2, false));
+  SQB_TRY(gram_wide_view(ctx, v, m, n, OP_SOLVE, s.r1, s.c2, false));
   if (allreduce) SQB_TRY(allreduce(s.c2));
   SQB_CUDA(launch_cholesky(s.c2, n, s.r2, ctx->d_status, ctx->stream));
   SQB_CUDA(launch_tri_multiply(s.r2, s.r1, n, d_r, ctx->stream));
@@ -240,14 +240,14 @@ int cholqr2_wide(sqb_context* ctx, const double* d_x, long long m, int n, long l
 }
 
 // SVQB2 beyond 64 columns (up to the reference's own eigh_small limit of 128, gram_qr.cpp:62).
-int svqb2_wide(sqb_context* ctx, const double* d_x, long long m, int n, long long ld, double* d_transform,
-               double* d_z, double* d_sigma, long long* d_rank, const std::function<int(double*)>& allreduce) {
+int svqb2_wide(sqb_context* ctx, const MatView& v, long long m, int n, double* d_transform, double* d_z,
+               double* d_sigma, long long* d_rank, const std::function<int(double*)>& allreduce) {
   Small s;
   SQB_TRY(small_slots(ctx, n, &s));
-  SQB_TRY(gram_wide_view(ctx, d_x, m, n, ld, OP_PLAIN, nullptr, s.c1, true));
+  SQB_TRY(gram_wide_view(ctx, v, m, n, OP_PLAIN, nullptr, s.c1, true));
   if (allreduce) SQB_TRY(allreduce(s.c1));
   SQB_CUDA(launch_svqb_pass(s.c1, n, s.b1, s.z1, d_sigma, s.rank1, 1, s.scratch, ctx->d_status, ctx->stream));
-  SQB_TRY(gram_wide_view(ctx, d_x, m, n, ld, OP_MULTIPLY, s.b1, s.c2, false));
+  SQB_TRY(gram_wide_view(ctx, v, m, n, OP_MULTIPLY, s.b1, s.c2, false));
   if (allreduce) SQB_TRY(allreduce(s.c2));
   SQB_CUDA(launch_svqb_pass(s.c2, n, s.b2, s.z2, s.s2, d_rank, 0, s.scratch, ctx->d_status, ctx->stream));
   SQB_CUDA(launch_small_multiply(s.b1, s.b2, n, d_transform, ctx->stream));
@@ -559,7 +559,8 @@ static int gram_entry(sqb_context* ctx, const double* d_x, int64_t m, int64_t n,
   if (n > 64) {
     // the reference's Gram kernels have no column limit (gram.cpp:113-151); here the plain Gram goes
     // up to 256 columns and the fused solve + Gram up to 128; the fused multiply stays at n <= 64
-    return gram_wide_view(ctx, d_x, m, static_cast<int>(n), ld, op, factor, d_c, op == OP_PLAIN);
+    return gram_wide_view(ctx, plain_view(d_x, ld, static_cast<int>(n)), m, static_cast<int>(n), op, factor, d_c,
+                          op == OP_PLAIN);
   }
   if (op == OP_MULTIPLY) {  // tsmmttsmm checks B for finiteness (gram.cpp:143-145)
     SQB_CUDA(launch_check_finite(factor, n * n, ctx->d_status, ctx->stream));
@@ -610,7 +611,7 @@ int sqb_cholqr2_dev(sqb_context* ctx, const double* d_x, int64_t m, int64_t n, i
                     int64_t num_blocks, int64_t panel_rows, double* d_r) {
   SQB_TRY(enter(ctx));
   SQB_TRY(check_shape(m, n, ld, kWideFusedMaxN));
-  if (n > 64) return cholqr2_wide(ctx, d_x, m, static_cast<int>(n), ld, d_r, nullptr);
+  if (n > 64) return cholqr2_wide(ctx, plain_view(d_x, ld, static_cast<int>(n)), m, static_cast<int>(n), d_r, nullptr);
   return cholqr2_view(ctx, plain_view(d_x, ld, static_cast<int>(n)), m, static_cast<int>(n), num_blocks,
                       panel_rows, d_r, nullptr);
 }
@@ -621,8 +622,8 @@ int sqb_svqb2_dev(sqb_context* ctx, const double* d_x, int64_t m, int64_t n, int
   SQB_TRY(enter(ctx));
   SQB_TRY(check_shape(m, n, ld, kWideFusedMaxN));
   if (n > 64)
-    return svqb2_wide(ctx, d_x, m, static_cast<int>(n), ld, d_transform, d_z, d_sigma,
-                      reinterpret_cast<long long*>(d_rank), nullptr);
+    return svqb2_wide(ctx, plain_view(d_x, ld, static_cast<int>(n)), m, static_cast<int>(n), d_transform, d_z,
+                      d_sigma, reinterpret_cast<long long*>(d_rank), nullptr);
   return svqb2_view(ctx, plain_view(d_x, ld, static_cast<int>(n)), m, static_cast<int>(n), num_blocks,
                     panel_rows, d_transform, d_z, d_sigma, reinterpret_cast<long long*>(d_rank),
                     nullptr);
@@ -663,6 +664,8 @@ int sqb_reconstruct_q_dev(sqb_context* ctx, const double* d_x, int64_t m, int64_
 
 static int lstsq_view(sqb_context* ctx, const MatView& v, int64_t m, int ne, int method,
                       double* d_xsol, double* d_residual, bool sharded) {
+  // [A rhs] may have up to 64 columns on the TSQR route (tsqr.cpp:188), up to 128 on the Gram routes
+  if (ne > (method == SQB_METHOD_TSQR ? 64 : kWideFusedMaxN)) return SQB_E_ARGUMENT;
   Small s;
   SQB_TRY(small_slots(ctx, ne, &s));
   double* r = s.rr;
@@ -672,10 +675,19 @@ static int lstsq_view(sqb_context* ctx, const MatView& v, int64_t m, int ne, int
     if (sharded) SQB_TRY(tsqr_sharded_view(ctx, v, m, ne, r));
     else SQB_TRY(tsqr_view(ctx, v, m, ne, 0, 0, r, true));
   } else if (method == SQB_METHOD_CHOLQR2) {
-    SQB_TRY(cholqr2_view(ctx, v, m, ne, 0, 0, r, ar));
+    if (ne > 64) SQB_TRY(cholqr2_wide(ctx, v, m, ne, r, ar));  // the Gram route has no 64-column limit
+    else SQB_TRY(cholqr2_view(ctx, v, m, ne, 0, 0, r, ar));
   } else if (method == SQB_METHOD_SVQB2) {
     // Z -> rr[0, ne^2), transform -> rr[ne^2, 2 ne^2) (svqb2_view owns every other slot)
     double* tr = s.rr + static_cast<size_t>(ne) * ne;
+    if (ne > 64) {
+      SQB_TRY(svqb2_wide(ctx, v, m, ne, tr, r, s.s2 + ne, s.rank1 + 1, ar));
+      SQB_CUDA(cudaMemcpyAsync(tr, r, sizeof(double) * ne * ne, cudaMemcpyDeviceToDevice, ctx->stream));
+      SQB_CUDA(launch_hhqr_small(tr, ne, r, ctx->stream));  // hhqr_small, lstsq.cpp:37-39
+      SQB_CUDA(launch_backsolve(r, ne, d_xsol, d_residual, ctx->d_status, ctx->stream));
+      ctx->launches += 2;
+      return SQB_OK;
+    }
     SQB_TRY(svqb2_view(ctx, v, m, ne, 0, 0, tr, r, s.s2 + ne, s.rank1 + 1, ar));
     // triangularise Z with the Householder kernel (reference hhqr_small, lstsq.cpp:37-39);
     // in-place is safe: the kernel stages Z on chip before writing its triangle.
@@ -693,7 +705,7 @@ int sqb_solve_lstsq_dev(sqb_context* ctx, const double* d_a, int64_t m, int64_t 
                         const double* d_rhs, int method, double* d_xsol, double* d_residual) {
   SQB_TRY(enter(ctx));
   if (n < 1 || m < n + 1) return SQB_E_DIMENSION;  // lstsq.cpp:16-17
-  if (n + 1 > 64 || lda < m) return SQB_E_ARGUMENT;
+  if (n + 1 > kWideFusedMaxN || lda < m) return SQB_E_ARGUMENT;
   const MatView v{d_a, lda, d_rhs, static_cast<int>(n)};
   return lstsq_view(ctx, v, m, static_cast<int>(n) + 1, method, d_xsol, d_residual, false);
 }
@@ -825,7 +837,7 @@ int sqb_cholqr2_host(sqb_context* ctx, const double* x, int64_t m, int64_t n, in
   Small s;
   SQB_TRY(small_slots(ctx, nn, &s));
   SQB_TRY(upload_slabs(ctx, x, m, nn, ld, 2, nullptr));
-  if (nn > 64) SQB_TRY(cholqr2_wide(ctx, ctx->xbuf, m, nn, m, s.rr, nullptr));
+  if (nn > 64) SQB_TRY(cholqr2_wide(ctx, plain_view(ctx->xbuf, m, nn), m, nn, s.rr, nullptr));
   else SQB_TRY(cholqr2_view(ctx, plain_view(ctx->xbuf, m, nn), m, nn, num_blocks, panel_rows, s.rr, nullptr));
   SQB_TRY(download(ctx, r, s.rr, sizeof(double) * nn * nn));
   return sqb_sync(ctx);
@@ -858,7 +870,7 @@ int sqb_svqb2_host(sqb_context* ctx, const double* x, int64_t m, int64_t n, int6
   SQB_TRY(small_slots(ctx, nn, &s));
   SQB_TRY(upload_slabs(ctx, x, m, nn, ld, 2, nullptr));
   if (nn > 64)
-    SQB_TRY(svqb2_wide(ctx, ctx->xbuf, m, nn, m, s.rr, s.rr + sq, s.s2 + nn, s.rank1 + 1, nullptr));
+    SQB_TRY(svqb2_wide(ctx, plain_view(ctx->xbuf, m, nn), m, nn, s.rr, s.rr + sq, s.s2 + nn, s.rank1 + 1, nullptr));
   else
     SQB_TRY(svqb2_view(ctx, plain_view(ctx->xbuf, m, nn), m, nn, num_blocks, panel_rows, s.rr, s.rr + sq,
                        s.s2 + nn, s.rank1 + 1, nullptr));
@@ -890,7 +902,7 @@ int sqb_solve_lstsq_host(sqb_context* ctx, const double* a, int64_t m, int64_t n
                          const double* rhs, int method, double* xsol, double* residual) {
   SQB_TRY(enter(ctx));
   if (n < 1 || m < n + 1) return SQB_E_DIMENSION;
-  if (n + 1 > 64 || lda < m) return SQB_E_ARGUMENT;
+  if (n + 1 > kWideFusedMaxN || lda < m) return SQB_E_ARGUMENT;
   const int nn = static_cast<int>(n);
   Small s;
   SQB_TRY(small_slots(ctx, nn + 1, &s));
@@ -978,7 +990,8 @@ int sqb_cholqr2_sharded_dev(sqb_context* ctx, const double* d_x, int64_t m_local
   if (n > kWideFusedMaxN || ld < m_local) return SQB_E_ARGUMENT;
   const int nn = static_cast<int>(n);
   if (nn > 64)
-    return cholqr2_wide(ctx, d_x, m_local, nn, ld, d_r, [ctx, nn](double* d) { return allreduce_square(ctx, d, nn); });
+    return cholqr2_wide(ctx, plain_view(d_x, ld, nn), m_local, nn, d_r,
+                        [ctx, nn](double* d) { return allreduce_square(ctx, d, nn); });
   return cholqr2_view(ctx, plain_view(d_x, ld, nn), m_local, nn, 0, 0, d_r,
                       [ctx, nn](double* d) { return allreduce_square(ctx, d, nn); });
 }
@@ -991,7 +1004,8 @@ int sqb_svqb2_sharded_dev(sqb_context* ctx, const double* d_x, int64_t m_local, 
   if (n > kWideFusedMaxN || ld < m_local) return SQB_E_ARGUMENT;
   const int nn = static_cast<int>(n);
   if (nn > 64)
-    return svqb2_wide(ctx, d_x, m_local, nn, ld, d_transform, d_z, d_sigma, reinterpret_cast<long long*>(d_rank),
+    return svqb2_wide(ctx, plain_view(d_x, ld, nn), m_local, nn, d_transform, d_z, d_sigma,
+                      reinterpret_cast<long long*>(d_rank),
                       [ctx, nn](double* d) { return allreduce_square(ctx, d, nn); });
   return svqb2_view(ctx, plain_view(d_x, ld, nn), m_local, nn, 0, 0, d_transform, d_z, d_sigma,
                     reinterpret_cast<long long*>(d_rank),
@@ -1003,7 +1017,7 @@ int sqb_solve_lstsq_sharded_dev(sqb_context* ctx, const double* d_a, int64_t m_l
                                 double* d_residual) {
   SQB_TRY(enter(ctx));
   if (n < 1 || m_local < 0) return SQB_E_DIMENSION;
-  if (n + 1 > 64 || lda < m_local) return SQB_E_ARGUMENT;
+  if (n + 1 > 64 || lda < m_local) return SQB_E_ARGUMENT;  // sharded least squares is the TSQR route
   const MatView v{d_a, lda, d_rhs, static_cast<int>(n)};
   return lstsq_view(ctx, v, m_local, static_cast<int>(n) + 1, SQB_METHOD_TSQR, d_xsol, d_residual,
                     true);

@@ -40,8 +40,8 @@ __device__ __forceinline__ void dmma_w(double& c0, double& c1, double a, double 
 }
 
 struct WideParams {
-  const double* x;
-  long long ld, m;
+  MatView x;  // columns [0, n_main) from base (leading dimension ld), the optional last one from `extra`
+  long long m;
   int n;
   int kb_tri, kb_full;  // row blocks per triangular / full chunk
   int nchunk;           // 128-column chunks (1 or 2)
@@ -57,7 +57,9 @@ __device__ __forceinline__ double2 frag(const double* stage, int tile, int t, in
 template <int W, int PP = kTriP, int ROWS = PP>
 __device__ __forceinline__ void tri_panel(const double* stage, double (&acc)[32][2], int g, int q) {
   constexpr int R1 = W, R2 = kWT - 1 - W;
-#pragma unroll
+  // the body is replicated once per warp (register-indexed accumulators): keep it to ONE row group per
+  // copy so that the eight variants stay resident in the instruction cache (ncu: no_instruction stalls)
+#pragma unroll 1
   for (int t = 0; t < ROWS / 8; ++t) {
     double2 b[kWT - R1];
 #pragma unroll
@@ -161,8 +163,9 @@ __global__ void __launch_bounds__(kWThreads, 1) gram_wide_kernel(const WideParam
   const long long begin = min(static_cast<long long>(rb) * rpb, prm.m);
   const long long end = min(static_cast<long long>(rb + 1) * rpb, prm.m);
   const long long npanels = (end - begin + kWP - 1) / kWP;
-  const bool aligned = ((reinterpret_cast<uintptr_t>(prm.x) & 15) == 0) && ((prm.ld & 1) == 0);
-  const double* colp = prm.x + static_cast<long long>(slot_ok ? col : 0) * prm.ld;
+  const bool aligned = (((reinterpret_cast<uintptr_t>(prm.x.base) | reinterpret_cast<uintptr_t>(prm.x.extra)) & 15) == 0) &&
+                       ((prm.x.ld & 1) == 0);
+  const double* colp = prm.x.col(slot_ok ? col : 0);
 
   double acc[32][2];
 #pragma unroll
@@ -437,8 +440,8 @@ __device__ __forceinline__ void solve_panel_out(const double* stage, const doubl
 }
 
 struct WideSolveParams {
-  const double* x;
-  long long ld, m;
+  MatView x;
+  long long m;
   int n, kb;
   const double* frags;  // U = R^-1 (rinv_wide_kernel) or B (bfrag_wide_kernel) in fragment order
   double* partial;      // one 128 x 128 column-major slab per CTA
@@ -473,8 +476,9 @@ __global__ void __launch_bounds__(kWThreads, 1) gram_wide_fused_kernel(const Wid
   const long long begin = min(static_cast<long long>(rb) * rpb, prm.m);
   const long long end = min(static_cast<long long>(rb + 1) * rpb, prm.m);
   const long long npanels = (end - begin + P - 1) / P;
-  const bool aligned = ((reinterpret_cast<uintptr_t>(prm.x) & 15) == 0) && ((prm.ld & 1) == 0);
-  const double* colp = prm.x + static_cast<long long>(slot_ok ? slot : 0) * prm.ld;
+  const bool aligned = (((reinterpret_cast<uintptr_t>(prm.x.base) | reinterpret_cast<uintptr_t>(prm.x.extra)) & 15) == 0) &&
+                       ((prm.x.ld & 1) == 0);
+  const double* colp = prm.x.col(slot_ok ? slot : 0);
 
   double acc[32][2];
 #pragma unroll
@@ -566,12 +570,11 @@ size_t gram_wide_partial_doubles(int n, int sm_count) {
   return static_cast<size_t>(sm_count + 2) * kWC * kWC;
 }
 
-cudaError_t launch_gram_wide(const double* x, long long m, int n, long long ld, int sm_count, double* partial,
+cudaError_t launch_gram_wide(const MatView& x, long long m, int n, int sm_count, double* partial,
                              double* c, int check_finite, StatusWord* status, cudaStream_t stream) {
   if (n <= 64 || n > kWideGramMaxN) return cudaErrorInvalidValue;
   WideParams prm;
   prm.x = x;
-  prm.ld = ld;
   prm.m = m;
   prm.n = n;
   prm.nchunk = (n + kWC - 1) / kWC;
@@ -582,8 +585,9 @@ cudaError_t launch_gram_wide(const double* x, long long m, int n, long long ld, 
     prm.kb_full = 0;
     grid = sm_count;
   } else {
-    // a full chunk costs 256 tile pairs, a triangular one 136: split the SMs in that ratio
-    prm.kb_full = (sm_count * 256 + 264) / 528;
+    // a full chunk costs 256 tile pairs, a triangular one 136 (and runs ~10 % faster per pair: taller
+    // panels, rolled row-group loop): split the SMs in that ratio
+    prm.kb_full = (sm_count * 256 + 250) / 500;
     prm.kb_tri = (sm_count - prm.kb_full) / 2;
     grid = 2 * prm.kb_tri + prm.kb_full;
   }
@@ -636,11 +640,10 @@ static cudaError_t launch_rinv_wide(const double* r, int n, double* frags, Statu
   return cudaGetLastError();
 }
 
-static WideSolveParams fused_params(const double* x, long long m, int n, long long ld, const double* frags,
-                                    int sm_count, int op) {
+static WideSolveParams fused_params(const MatView& x, long long m, int n, const double* frags, int sm_count,
+                                    int op) {
   WideSolveParams prm;
   prm.x = x;
-  prm.ld = ld;
   prm.m = m;
   prm.n = n;
   prm.frags = frags;
@@ -652,7 +655,7 @@ static WideSolveParams fused_params(const double* x, long long m, int n, long lo
   return prm;
 }
 
-cudaError_t launch_gram_wide_fused(const double* x, long long m, int n, long long ld, int op, const double* factor,
+cudaError_t launch_gram_wide_fused(const MatView& x, long long m, int n, int op, const double* factor,
                                    int sm_count, double* frags, double* partial, double* c, StatusWord* status,
                                    cudaStream_t stream) {
   if (n <= 64 || n > kWideFusedMaxN || (op != OP_SOLVE && op != OP_MULTIPLY)) return cudaErrorInvalidValue;
@@ -664,7 +667,7 @@ cudaError_t launch_gram_wide_fused(const double* x, long long m, int n, long lon
     e = cudaGetLastError();
   }
   if (e != cudaSuccess) return e;
-  WideSolveParams prm = fused_params(x, m, n, ld, frags, sm_count, op);
+  WideSolveParams prm = fused_params(x, m, n, frags, sm_count, op);
   prm.partial = partial;
   e = op == OP_SOLVE ? launch_fused<OP_SOLVE>(prm, stream) : launch_fused<OP_MULTIPLY>(prm, stream);
   if (e != cudaSuccess) return e;
@@ -680,7 +683,7 @@ cudaError_t launch_apply_rinv_wide(const double* x, long long m, int n, long lon
   if (n <= 64 || n > kWideFusedMaxN) return cudaErrorInvalidValue;
   cudaError_t e = launch_rinv_wide(r, n, frags, status, stream);
   if (e != cudaSuccess) return e;
-  WideSolveParams prm = fused_params(x, m, n, ld, frags, sm_count, OP_SOLVE);
+  WideSolveParams prm = fused_params(MatView{x, ld, nullptr, n}, m, n, frags, sm_count, OP_SOLVE);
   prm.qout = q;
   prm.ldq = ldq;
   return launch_fused<OP_SOLVE, true>(prm, stream);

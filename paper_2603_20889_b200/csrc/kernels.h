@@ -119,14 +119,14 @@ int gram_ctas_per_sm(int n, int op);
 // ---- gram_wide_kernels.cu (64 < n <= 256, plain Gram only: BASELINE config 5) -----------------
 constexpr int kWideGramMaxN = 256;
 size_t gram_wide_partial_doubles(int n, int sm_count);
-cudaError_t launch_gram_wide(const double* x, long long m, int n, long long ld, int sm_count, double* partial,
+cudaError_t launch_gram_wide(const MatView& x, long long m, int n, int sm_count, double* partial,
                              double* c, int check_finite, StatusWord* status, cudaStream_t stream);
 
 // fused solve / multiply + Gram (the second CholQR2 / SVQB2 sweep) for 64 < n <= 128;
 // frags: gram_wide_fused_scratch_doubles() doubles of device scratch
 constexpr int kWideFusedMaxN = 128;
 size_t gram_wide_fused_scratch_doubles();
-cudaError_t launch_gram_wide_fused(const double* x, long long m, int n, long long ld, int op, const double* factor,
+cudaError_t launch_gram_wide_fused(const MatView& x, long long m, int n, int op, const double* factor,
                                    int sm_count, double* frags, double* partial, double* c, StatusWord* status,
                                    cudaStream_t stream);
 
@@ -156,6 +156,8 @@ cudaError_t launch_tri_multiply(const double* a, const double* b, int n, double*
                                 cudaStream_t stream);
 cudaError_t launch_small_multiply(const double* a, const double* b, int n, double* out,
                                   cudaStream_t stream);
+// Householder QR of an n x n matrix, n <= 128 (reference hhqr_small in solve_lstsq's SVQB2 route, lstsq.cpp:37-39)
+cudaError_t launch_hhqr_small(const double* z, int n, double* r, cudaStream_t stream);
 cudaError_t launch_backsolve(const double* r, int ne, double* xsol, double* residual,
                              StatusWord* status, cudaStream_t stream);
 cudaError_t launch_check_finite(const double* a, long long count, StatusWord* status,

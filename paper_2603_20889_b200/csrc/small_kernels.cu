@@ -433,6 +433,53 @@ __global__ void small_multiply_kernel(const double* __restrict__ a, const double
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// Householder QR of a small n x n matrix (reference hhqr_small as used by solve_lstsq's SVQB2 route,
+// lstsq.cpp:37-39), n <= 128, one CTA: the 65..128-column complement of the streaming TSQR kernels
+// (which stop at 64 columns like tsqr.cpp:188).  Same reflector convention (make_reflector), R is
+// sign-normalised (types.cpp:8-14) and its strict lower triangle is exact zero.
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSmallThreads)
+    hhqr_small_kernel(const double* __restrict__ z, int n, double* __restrict__ r) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double red[kSmallThreads];
+  __shared__ Reflector hs;
+  const int ld = n + 1;
+  double* a = sm;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int idx = tid; idx < n * n; idx += kSmallThreads) a[idx % n + (idx / n) * ld] = z[idx];
+  __syncthreads();
+  for (int c = 0; c < n; ++c) {
+    double sg = 0.0;
+    for (int i = c + 1 + tid; i < n; i += kSmallThreads) sg = fma(a[i + c * ld], a[i + c * ld], sg);
+    const double sigma = block_sum(sg, red);
+    if (tid == 0) hs = make_reflector(a[c + c * ld], sigma);
+    __syncthreads();
+    const Reflector h = hs;
+    for (int j = c + 1 + warp; j < n; j += kSmallThreads / 32) {  // a warp per trailing column
+      double d = 0.0;
+      for (int i = c + 1 + lane; i < n; i += 32) d = fma(a[i + c * ld], a[i + j * ld], d);
+      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      d = h.gamma * fma(h.u0, a[c + j * ld], d);
+      for (int i = c + 1 + lane; i < n; i += 32) a[i + j * ld] = fma(-d, a[i + c * ld], a[i + j * ld]);
+      __syncwarp();
+      if (lane == 0) a[c + j * ld] = fma(-d, h.u0, a[c + j * ld]);
+    }
+    __syncthreads();
+    if (tid == 0) a[c + c * ld] = h.beta;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < n * n; idx += kSmallThreads) {
+    const int i = idx % n, j = idx / n;
+    double v = 0.0;
+    if (i <= j) {
+      v = a[i + j * ld];
+      if (a[i + i * ld] < 0.0) v = -v;
+    }
+    r[idx] = v;
+  }
+}
+
 // Least-squares tail (lstsq.cpp:44-59): back-substitution on the leading n x n block of the
 // (n+1) x (n+1) triangle of [A rhs]; residual = |R(n,n)|; RankDeficiencyError(i) when
 // |R(i,i)| <= n*eps*max|diag R[0:n]|.
@@ -560,6 +607,15 @@ cudaError_t launch_tri_multiply(const double* a, const double* b, int n, double*
 cudaError_t launch_small_multiply(const double* a, const double* b, int n, double* out,
                                   cudaStream_t stream) {
   small_multiply_kernel<<<1, 256, 0, stream>>>(a, b, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hhqr_small(const double* z, int n, double* r, cudaStream_t stream) {
+  if (n < 1 || n > kSmallMaxN) return cudaErrorInvalidValue;
+  const size_t bytes = sizeof(double) * static_cast<size_t>(n) * (n + 1);
+  cudaError_t e = opt_in_smem(hhqr_small_kernel, bytes);
+  if (e != cudaSuccess) return e;
+  hhqr_small_kernel<<<1, kSmallThreads, bytes, stream>>>(z, n, r);
   return cudaGetLastError();
 }
 

@@ -337,6 +337,30 @@ def test_solve_lstsq(ctx, oracle, method, m, n):
     assert abs(res - res_ref) <= 1e-10 * res_ref
 
 
+@pytest.mark.parametrize("m,n", [(9000, 64), (12000, 100), (6001, 127)])
+def test_solve_lstsq_wide_gram_routes(ctx, sq, oracle, m, n):
+    """[A rhs] with 65..128 columns: the CholQR2 / SVQB2 routes have no 64-column limit in the reference
+    (lstsq.cpp:31-39); rhs stays a separate array (last column of the wide kernels' view)."""
+    import torch
+    a = gaussian(m, n, seed=n + 1)
+    rhs = a @ np.arange(1, n + 1, dtype=np.float64) + 0.01 * gaussian(m, 1, seed=78)[:, 0]
+    xs, res = ctx.solve_lstsq(a, rhs, "cholqr2")
+    xs_ref, res_ref = oracle.port.solve_lstsq(a, rhs, "cholqr2")
+    assert np.linalg.norm(xs - xs_ref) <= 1e-10 * np.linalg.norm(xs_ref)
+    assert abs(res - res_ref) <= 1e-10 * res_ref
+    ad = torch.from_numpy(np.ascontiguousarray(a.T)).cuda().t()
+    xd, rd = ctx.solve_lstsq(ad, torch.from_numpy(rhs).cuda(), "cholqr2")
+    ctx.synchronize()
+    assert np.linalg.norm(xd.cpu().numpy() - xs_ref) <= 1e-10 * np.linalg.norm(xs_ref)
+    assert abs(float(rd) - res_ref) <= 1e-10 * res_ref
+    xv, rv = ctx.solve_lstsq(a, rhs, "svqb2")
+    xv_ref, rv_ref = oracle.port.solve_lstsq(a, rhs, "svqb2")
+    assert np.linalg.norm(xv - xv_ref) <= 1e-9 * np.linalg.norm(xv_ref)
+    assert abs(rv - rv_ref) <= 1e-9 * rv_ref
+    with pytest.raises(sq.ArgumentError):  # tsqr.cpp:188
+        ctx.solve_lstsq(a, rhs, "tsqr")
+
+
 def test_lstsq_rank_deficient(ctx, sq):
     a = gaussian(400, 3, seed=1)
     a[:, 2] = 0.0
