@@ -28,10 +28,10 @@ constexpr int kWC = 8 * kWT;     // columns per chunk (128)
 // panel rows == stage pitch == 8 (mod 16): conflict-free LDS.128 fragment reads without padding.  The
 // triangular chunk stages 128 columns, the full one 256, so the former affords taller panels (fewer
 // CTA barriers per row) in the same shared memory.
-constexpr int kTriP = 40;
+constexpr int kTriP = 56;
 constexpr int kFullP = 24;
 constexpr int kWThreads = 256;   // 8 warps
-constexpr int kWStages = 4;      // panels in flight (HBM latency is ~2 panel times)
+constexpr int kWStages = 3;      // panels in flight (a panel is several us of DMMAs: far more than the HBM latency)
 
 __device__ __forceinline__ void dmma_w(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
