@@ -512,9 +512,9 @@ int sqb_default_tsqr_plan(const sqb_context* ctx, int64_t m, int64_t n, int64_t*
 int sqb_default_gram_plan(const sqb_context* ctx, int64_t m, int64_t n, int64_t* num_blocks,
                           int64_t* panel_rows) {
   if (!ctx || n < 1 || n > kWideGramMaxN) return SQB_E_ARGUMENT;  // plan.cpp:9-17 has no column limit
-  if (n > 64) {  // the wide kernel partitions rows itself: report its shape (one row block per SM, 40-row panels)
+  if (n > 64) {  // the wide kernel partitions rows itself: report its shape (one row block per SM, 56-row panels)
     if (num_blocks) *num_blocks = ctx->sm_count;
-    if (panel_rows) *panel_rows = 40;
+    if (panel_rows) *panel_rows = 56;
     return SQB_OK;
   }
   const Plan p = gram_plan(ctx, m, static_cast<int>(n), OP_PLAIN, 0, 0);

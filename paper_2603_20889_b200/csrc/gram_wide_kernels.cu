@@ -9,7 +9,7 @@
 //     pair (ci <= cj) and one row block; n = 128 is a single triangular chunk, n = 256 is two
 //     triangular chunks plus one full off-diagonal chunk - 32.9 K accumulators do not fit one SM's
 //     register file, so the off-diagonal chunk gets its own CTAs (and re-reads its 256 columns).
-//   * the CTA streams P-row panels of the chunk's columns through a 4-stage shared-memory
+//   * the CTA streams P-row panels of the chunk's columns through a 3-stage shared-memory
 //     stage (cp.async.bulk per column segment, one mbarrier per stage, every thread issues one copy);
 //   * every warp owns fixed tile pairs in registers for the whole row block - triangular chunk: tile
 //     rows w and 15-w (17 pairs per warp, perfectly balanced); full chunk: tile rows 2w, 2w+1 against
