@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(kWThreads, 1) gram_wide_kernel(const WideParam
 // The reference substitutes column by column inside a cache-resident panel; a column-sequential
 // substitution across 128 columns would serialise the eight warps of a CTA, so here the triangular
 // solve is turned into a tensor-core GEMM with the explicit inverse U = R^-1 (rinv_wide_kernel, one
-// CTA, 40 us): per 24-row panel
+// CTA, 40 us): per 32-row panel
 //     Q^T tile (8 columns j x 8 rows)  =  sum_{k <= j}  U^T[8j.., 4k..] * X^T[4k.., rows]     (DMMA)
 // whose accumulator fragment (lane (g,q): Q[row 2q+e, column 8j+g]) is exactly the operand layout of
 // the SYRK (tri_panel), so it goes to a shared Q panel with one conflict-free 128-bit store and the
@@ -261,20 +261,22 @@ __global__ void __launch_bounds__(kWThreads, 1) gram_wide_kernel(const WideParam
 // Panel geometry per variant.  The solve GEMM reads the X stage with the transposed LDS.64 pattern
 // ((4k+q) * pitch + 8t + g): conflict-free for pitch = 4 or 12 (mod 16); the SYRK reads the Q panel with
 // the LDS.128 pattern ((8T+g) * pitch + 8t + 2q): conflict-free for pitch = 8 (mod 16).
-__host__ __device__ constexpr int fused_rows(int op) { return op == OP_SOLVE ? 24 : 16; }
-__host__ __device__ constexpr int fused_spitch(int op) { return op == OP_SOLVE ? 28 : 20; }
-constexpr int kQPitch = 24;
+__host__ __device__ constexpr int fused_rows(int op) { return op == OP_SOLVE ? 32 : 16; }
+__host__ __device__ constexpr int fused_spitch(int op) { return op == OP_SOLVE ? 36 : 20; }
+__host__ __device__ constexpr int fused_qpitch(int op) { return op == OP_SOLVE ? 40 : 24; }
 // k4 steps per warp: triangular factor (OP_SOLVE, U = R^-1) (2w+2) + (32-2w) = 34; dense factor
 // (OP_MULTIPLY, B) 32 + 32
 __host__ __device__ constexpr int fused_ksteps(int op) { return op == OP_SOLVE ? 34 : 64; }
 __host__ __device__ constexpr int fused_k1(int op, int w) { return op == OP_SOLVE ? 2 * w + 2 : 32; }
 __host__ __device__ constexpr int fused_k2(int op, int w) { return op == OP_SOLVE ? 2 * (kWT - 1 - w) + 2 : 32; }
 __host__ __device__ constexpr int fused_frag_doubles(int op) { return 8 * fused_ksteps(op) * 32; }
-// panels in flight: the fused passes are far on the tensor-pipe side (a panel is ~5 us of DMMAs), so the
-// dense factor's 128 KB of fragments may squeeze the ring down to two stages
-__host__ __device__ constexpr int fused_stages(int op) { return op == OP_SOLVE ? 3 : 2; }
+// panels in flight: the fused passes are far on the tensor-pipe side (a panel is ~5 us of DMMAs), so a
+// two-stage ring is enough; the shared memory goes to taller panels (solve) / the dense factor's 128 KB
+// of fragments (multiply) instead
+__host__ __device__ constexpr int fused_stages(int) { return 2; }
 __host__ __device__ constexpr size_t fused_smem_doubles(int op) {
-  return static_cast<size_t>(fused_stages(op)) * kWC * fused_spitch(op) + 2 * kWC * kQPitch + fused_frag_doubles(op);
+  return static_cast<size_t>(fused_stages(op)) * kWC * fused_spitch(op) + 2 * kWC * fused_qpitch(op) +
+         fused_frag_doubles(op);
 }
 constexpr double kEpsW = 2.220446049250313e-16;
 
@@ -406,14 +408,14 @@ __device__ __forceinline__ void solve_tiles(const double* stage, const double* r
 template <int OP>
 __device__ __forceinline__ void solve_panel(const double* stage, const double* rf, double* qb, int n, int w,
                                             int lane, int g, int q) {
-  constexpr int NT = fused_rows(OP) / 8;
+  constexpr int NT = fused_rows(OP) / 8, QP = fused_qpitch(OP);
   const int j1 = w, j2 = kWT - 1 - w;
   double a1c[NT][2], a2c[NT][2];
   solve_tiles<OP>(stage, rf, a1c, a2c, w, (n + 3) / 4, lane, g, q);
 #pragma unroll
   for (int t = 0; t < NT; ++t) {
-    *reinterpret_cast<double2*>(qb + (8 * j1 + g) * kQPitch + 8 * t + 2 * q) = make_double2(a1c[t][0], a1c[t][1]);
-    *reinterpret_cast<double2*>(qb + (8 * j2 + g) * kQPitch + 8 * t + 2 * q) = make_double2(a2c[t][0], a2c[t][1]);
+    *reinterpret_cast<double2*>(qb + (8 * j1 + g) * QP + 8 * t + 2 * q) = make_double2(a1c[t][0], a1c[t][1]);
+    *reinterpret_cast<double2*>(qb + (8 * j2 + g) * QP + 8 * t + 2 * q) = make_double2(a2c[t][0], a2c[t][1]);
   }
 }
 
@@ -454,6 +456,7 @@ __global__ void __launch_bounds__(kWThreads, 1) gram_wide_fused_kernel(const Wid
   extern __shared__ __align__(128) double smem[];
   constexpr int NSTAGE = fused_stages(OP), P = fused_rows(OP), SP = fused_spitch(OP);
   __shared__ uint64_t bars[NSTAGE];
+  constexpr int kQPitch = fused_qpitch(OP);
   constexpr int kStageDoubles = kWC * SP, kQDoubles = kWC * kQPitch;
   double* qbuf = smem + NSTAGE * kStageDoubles;  // two Q panels
   double* rf = qbuf + 2 * kQDoubles;             // factor fragments
