@@ -203,5 +203,8 @@ if alln.exists():
 san = G / f"{tag}_sanitizer.txt"
 if san.exists():
     out.append(f"\n## compute-sanitizer (memcheck on the GPU parity suite, racecheck on the Gram / TSQR parity tests)\n\n```\n{san.read_text().strip()}\n```")
+rw = G / f"{tag}_race_wide.txt"
+if rw.exists():
+    out.append(f"\nRe-run on the final fused-kernel geometry (32-row solve panels, 2-stage ring):\n\n```\n{rw.read_text().strip()}\n```")
 (P / "README.md").write_text("\n".join(out) + "\n")
 print("wrote", P / "README.md")

@@ -18,3 +18,5 @@ prof3 gram_wide_multiply_n128 svqb2
 python tools/time_gram_wide.py 24 > $O/${TAG}_wide.txt 2>&1
 python tools/run_configs.py $TAG > $O/${TAG}_configs.log 2>&1
 python -m pytest tests -m gpu -q 2>&1 | tail -3 > $O/${TAG}_gpu_tests.txt
+echo 'compute-sanitizer --tool racecheck python -m pytest tests/test_gpu_parity.py -m gpu -k "300-128"   (final fused-kernel geometry)' > $O/${TAG}_race_wide.txt
+timeout 800 compute-sanitizer --tool racecheck python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "300-128" 2>&1 | tail -2 >> $O/${TAG}_race_wide.txt
