@@ -2,23 +2,31 @@
 """Benchmark of the Q-less tall-skinny QR hot path (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--n COLS] [--m ROWS] [--no-sweep]
+    python bench.py --config c4 [--gpus N]    # BASELINE configs[3]: 1e9 x 16 [A b] least squares, strong scaling
     python bench.py --impl reference ...      # the reference's CPU implementation, host cores
 
 Metric: Q-less QR effective HBM GB/s = 8*m*n / t (one logical read of X).  One "step" is one
 Q-less TSQR factorisation (sqb_tsqr_qless_dev: the streaming kernel + the R-factor combine) of
 an m x n FP64 Gaussian matrix that is already resident in HBM.  Workload = BASELINE.json
-configs[1] (single-B200 column sweep at m = 2^27): the headline `value` is the n = 8 point of the
-sweep, the whole sweep (n = 1..64, TSQR / CholQR2 / SVQB2) is attached as "sweep".  X (n GiB) is
-far larger than the 126 MB L2, so every step streams from HBM.
+configs[1] (single-B200 column sweep at m = 2^27): the headline is the n = 8 point of the sweep,
+the whole sweep (n = 1..64, TSQR / CholQR2 / SVQB2) is attached as "sweep".  X (n GiB) is far
+larger than the 126 MB L2, so every step streams from HBM.
 
-N > 1 (torchrun, one process per GPU): rows are sharded, each rank factors its own 2^27-row slab
-and the n x n triangles are combined with an NCCL all-gather (weak scaling).
+`value` is the SUSTAINED figure: K steps timed after 300 ms of untimed back-to-back steps, i.e.
+with the board on its power cap; `burst` is the same K steps on a settled (idle) board.
+
+N > 1: `--gpus N` without a torchrun environment re-executes this script under
+`python -m torch.distributed.run --nproc-per-node N` (one process per GPU); under the driver's own
+torchrun the ranks are used as given.  Rows are sharded: each rank factors its own 2^27-row slab and
+the n x n triangles are combined with an NCCL all-gather inside the library (weak scaling).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
+import subprocess
 import sys
 import threading
 import time
@@ -29,6 +37,8 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "Q-less QR effective HBM GB/s (8*m*n bytes / time-to-solution), FP64"
 NOMINAL_HBM_GBS = 8000.0
+FP64_PEAK_TFLOPS = 36.9   # measured DFMA / DMMA peak at 1.965 GHz (tools/probe_fp64.cu, profiles/probes/)
+READ_CEILING_GBS = 7400.0  # measured read-only stream (tools/probe.cu)
 
 
 def measured_peaks():
@@ -37,6 +47,18 @@ def measured_peaks():
         d = json.loads(p.read_text())
         return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json, copy bandwidth)"
     return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def spawn_command(n_gpus, argv, port):
+    """The command `--gpus N` re-executes when no torchrun environment is present."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n_gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py")] + list(argv)
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 class ClockSampler(threading.Thread):
@@ -80,6 +102,15 @@ class ClockSampler(threading.Thread):
                 "reasons": sorted(self.reasons), "samples": len(s)}
 
 
+def roofline_bound(method, m, n, hbm_peak_gbs):
+    """Which roofline binds one streaming pass: 8mn bytes over HBM against the pass's FP64 flops at
+    the measured FP64 peak (TSQR 2mn^2; Gram mn(n+1) executed, gram.cpp:118-119)."""
+    t_hbm = 8.0 * m * n / (hbm_peak_gbs * 1e9)
+    flops = 2.0 * m * n * n if method == "tsqr" else float(m) * n * (n + 1)
+    t_fp = flops / (FP64_PEAK_TFLOPS * 1e12)
+    return ("hbm", t_hbm, flops) if t_hbm >= t_fp else ("fp64", t_fp, flops)
+
+
 def cpu_reference_run(m, n, steps, warmup, method="tsqr", x_host=None):
     """Times the reference's own CPU implementation (oracle/_ref when built, else the C port) on
     the host cores.  Returns (best GB/s, mean GB/s, description dict)."""
@@ -90,7 +121,17 @@ def cpu_reference_run(m, n, steps, warmup, method="tsqr", x_host=None):
     if oracle.ref is not None:
         ref = oracle.ref
         h, view = ref.matrix_handle(m, n)
-        view[:, :] = x_host if x_host is not None else oracle.gaussian(m, n, 1234)
+        if x_host is not None:
+            view[:, :] = x_host
+            gen = "rows of the GPU arm's matrix"
+        elif m * n <= (1 << 24):
+            view[:, :] = oracle.gaussian(m, n, 1234)
+            gen = "counter-based Gaussian, seed 1234"
+        else:  # large samples: numpy's generator straight into the reference's buffer, column by column
+            rng = np.random.default_rng(1234)
+            for j in range(n):
+                rng.standard_normal(m, out=view[:, j])
+            gen = "numpy standard_normal, seed 1234"
         for _ in range(warmup):
             ref.timed(h, method, n)
         ts = [ref.timed(h, method, n)[0] for _ in range(steps)]
@@ -101,6 +142,7 @@ def cpu_reference_run(m, n, steps, warmup, method="tsqr", x_host=None):
             info["value_without_validation_scan"] = nbytes / min(ts_nv) / 1e9
     else:
         x = x_host if x_host is not None else oracle.gaussian(m, n, 1234)
+        gen = "counter-based Gaussian, seed 1234"
         fn = {"tsqr": oracle.port.tsqr_qless, "cholqr2": oracle.port.cholqr2}[method]
         for _ in range(warmup):
             fn(x)
@@ -110,8 +152,25 @@ def cpu_reference_run(m, n, steps, warmup, method="tsqr", x_host=None):
             fn(x)
             ts.append(time.perf_counter() - t0)
         info = {"kind": "port", "cores": 1}
-    info["sample"] = f"{method} of a {m} x {n} FP64 Gaussian ({nbytes / 2**30:.2f} GiB), {steps} timed calls"
+    info["sample"] = (f"{method} of a {m} x {n} FP64 Gaussian ({nbytes / 2**30:.2f} GiB; {gen}), "
+                      f"{steps} timed calls after {warmup} warm-ups")
     return nbytes / min(ts) / 1e9, nbytes * len(ts) / sum(ts) / 1e9, info
+
+
+def reference_rows(m, n, requested):
+    """Rows of the reference arm's matrix: the GPU arm's own m when the host has room for it
+    (matrix + the reference's workspaces + slack), otherwise the largest power of two that fits."""
+    if requested:
+        return int(requested)
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 8 << 30
+    rows = m
+    while rows > 1024 and 8 * rows * n * 1.5 + (2 << 30) > avail:
+        rows //= 2
+    return rows
 
 
 def run_reference_arm(args):
@@ -119,79 +178,62 @@ def run_reference_arm(args):
     if rank != 0:
         return
     n = args.n
-    m = args.cpu_rows or (1 << 27) // max(n, 8)
+    m = reference_rows(args.m, n, args.cpu_rows)
     best, mean, info = cpu_reference_run(m, n, args.steps, args.warmup)
     t_ms = 8.0 * m * n / (mean * 1e9) * 1e3
     info["value"] = mean
     info["unit"] = "GB/s"
+    same = m == args.m
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": mean, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"tsqr_qless m=2^27 n={n} (BASELINE configs[1]); reference CPU path on a "
-                               f"bounded {m}-row sample of it", "m": m, "n": n},
+        "config": {"workload": f"tsqr_qless m=2^27 n={n} (BASELINE configs[1]); reference CPU path "
+                               + ("at the GPU arm's full size" if same else f"on a bounded {m}-row sample of it"),
+                   "m": m, "n": n, "same_config": same},
         "cpu_baseline": info, "best_gbs": best,
         "e2e": {"value": mean, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=8, help="columns of the headline workload")
-    ap.add_argument("--m", type=int, default=1 << 27, help="rows per GPU")
-    ap.add_argument("--method", default="tsqr", choices=["tsqr", "cholqr2", "svqb2"])
-    ap.add_argument("--no-sweep", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--sweep-reps", type=int, default=5)
-    ap.add_argument("--cpu-rows", type=int, default=0)
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
-    if args.impl == "reference":
-        return run_reference_arm(args)
+class Rig:
+    """One rank's device, context and process group."""
 
-    import numpy as np
-    import torch
-    import paper_2603_20889_b200 as sq
+    def __init__(self):
+        import torch
+        import paper_2603_20889_b200 as sq
+        from paper_2603_20889_b200 import sharding
+        self.torch, self.sq, self.sharding = torch, sq, sharding
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(self.local)
+        self.dev = torch.device(f"cuda:{self.local}")
+        self.dist = None
+        self.transport = None
+        self.ctx = sq.Context(self.local)
+        self.ctx.use_torch_stream()
+        if self.world > 1:
+            import torch.distributed as dist
+            os.environ.setdefault("NCCL_DEBUG", "INFO" if self.rank == 0 else "WARN")  # communicator log stays on
+            dist.init_process_group("nccl", device_id=self.dev)
+            self.dist = dist
+            self.transport = sharding.attach(self.ctx, dist)  # the library's own NCCL communicator
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    ctx = sq.Context(local)
-    ctx.use_torch_stream()
-    if world > 1:
-        box = [ctx.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(box, src=0)
-        ctx.init_nccl(box[0], rank, world)
+    def sync_all(self):
+        self.torch.cuda.synchronize()
+        if self.dist is not None:
+            self.dist.barrier()
+            self.torch.cuda.synchronize()
 
-    m, n = args.m, args.n
-    dev = torch.device(f"cuda:{local}")
+    def max_ranks(self, v):
+        return self.sharding.max_over_ranks(v, self.dist) if self.dist is not None else float(v)
 
-    def sync_all():
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
-            torch.cuda.synchronize()
-
-    def run_method(x, method):
-        if method == "tsqr":
-            return ctx.tsqr_qless_sharded(x) if world > 1 else ctx.tsqr_qless(x)
-        if method == "cholqr2":
-            return ctx.cholqr2_sharded(x) if world > 1 else ctx.cholqr2(x)
-        return ctx.svqb2_sharded(x) if world > 1 else ctx.svqb2(x)
-
-    def timed(fn, steps, warmup, spinup_ms=0.0):
-        # optional untimed spin-up so that the timed region starts at steady clocks (a 1.4 ms step
-        # times 3 warm-ups is over before the SM clock has ramped), then the W warm-up steps proper
+    def timed(self, fn, steps, warmup, spinup_ms=0.0):
+        """W warm-ups, then exactly K steps between CUDA events on the launching stream, bracketed by
+        barrier + synchronize; max over ranks.  spinup_ms > 0 first runs untimed back-to-back steps so
+        that the timed region starts with the board already on its sustained clocks."""
+        torch, ctx = self.torch, self.ctx
         if spinup_ms > 0.0:
             t_end = time.perf_counter() + spinup_ms * 1e-3
             while time.perf_counter() < t_end:
@@ -200,36 +242,60 @@ def main():
                 torch.cuda.synchronize()
         for _ in range(warmup):
             fn()
-        sync_all()
+        self.sync_all()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         l0 = ctx.launch_count
         e0.record()
         for _ in range(steps):
             fn()
         e1.record()
-        sync_all()
+        self.sync_all()
         ctx.synchronize("bench")  # surfaces device-side numerical failures
-        ms = e0.elapsed_time(e1)
-        if dist is not None:
-            t = torch.tensor([ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms / steps, ctx.launch_count - l0
+        return self.max_ranks(e0.elapsed_time(e1)) / steps, ctx.launch_count - l0
 
-    # ---- headline: whole-job throughput, inputs resident in HBM ------------------------------
+    def close(self):
+        if self.dist is not None:
+            self.dist.destroy_process_group()
+
+
+def traffic_per_launch(method, n, m):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full captures
+    (profiles/traffic.json: bytes measured at `m` rows), scaled to this run's row count."""
+    tfile = ROOT / "profiles" / "traffic.json"
+    try:
+        ent = json.loads(tfile.read_text()).get(f"{method}_n{n}")
+        return float(ent["bytes"]) * m / float(ent["m"]) if ent else None
+    except Exception:
+        return None
+
+
+def run_headline(rig, args):
+    import numpy as np
+    torch, sq, ctx = rig.torch, rig.sq, rig.ctx
+    rank, world, local, dev = rig.rank, rig.world, rig.local, rig.dev
+    m, n = args.m, args.n
+
+    def run_method(x, method):
+        if method == "tsqr":
+            return ctx.tsqr_qless_sharded(x) if world > 1 else ctx.tsqr_qless(x)
+        if method == "cholqr2":
+            return ctx.cholqr2_sharded(x) if world > 1 else ctx.cholqr2(x)
+        return ctx.svqb2_sharded(x) if world > 1 else ctx.svqb2(x)
+
+    # ---- burst: K steps on a settled board, inputs resident in HBM ---------------------------------
     x = ctx.fill_gaussian(m, n, seed=1234, row_offset=rank * m, m_total=world * m)
-    # the generator kernel (log/cos heavy) runs into the 1 kW power cap; let the board settle so the
-    # timed region measures the TSQR step, not the generator's thermal tail
+    # the generator kernel (log/cos heavy) runs into the 1 kW power cap; let the board settle first
     torch.cuda.synchronize()
     time.sleep(1.0)
     sampler = ClockSampler(local)
     sampler.start()
-    ms_step, launches = timed(lambda: run_method(x, args.method), args.steps, args.warmup)
-    clocks = sampler.stop()
+    ms_burst, _ = rig.timed(lambda: run_method(x, args.method), args.steps, args.warmup)
+    clocks_burst = sampler.stop()
     total_bytes = 8.0 * m * n * world
-    value = total_bytes / (ms_step * 1e-3) / 1e9
+    burst = total_bytes / (ms_burst * 1e-3) / 1e9
+
     # ---- dominant kernel (the streaming launch that reads X once) timed IN SITU for the roofline:
-    # the same step as above issued as its two launches, CUDA events bracketing the first one only
+    # the same step issued as its two launches, CUDA events bracketing the first one only
     peak, peak_src = measured_peaks()
     plan = ctx.default_tsqr_plan(m, n) if args.method == "tsqr" else ctx.default_gram_plan(m, n)
     lib, I64, vp = ctx.lib, sq.I64, ctx._ptr
@@ -257,11 +323,11 @@ def main():
         def rest_of_step():
             ctx.cholesky(c_out)
         kname = "gram kernel (first streaming pass) + gram_reduce_kernel"
-    time.sleep(0.5)  # same board state as the headline: settled, not on the power cap
+    time.sleep(0.5)  # settled board, like the burst figure
     for _ in range(args.warmup):
         stream_launch()
         rest_of_step()
-    sync_all()
+    rig.sync_all()
     pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
              for _ in range(args.steps)]
     for e0, e1 in pairs:
@@ -269,48 +335,52 @@ def main():
         stream_launch()
         e1.record()
         rest_of_step()
-    sync_all()
+    rig.sync_all()
     try:
         ctx.synchronize("bench")
     except sq.Error:
         pass
-    ms_kernel = sum(a.elapsed_time(b) for a, b in pairs) / len(pairs)
-    if dist is not None:
-        t = torch.tensor([ms_kernel], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_kernel = float(t.item())
-    achieved = 8.0 * m * n / (ms_kernel * 1e-3) / 1e9
-    traffic = None
-    tfile = ROOT / "profiles" / "traffic.json"
-    if tfile.exists():
-        try:
-            traffic = json.loads(tfile.read_text()).get(f"{args.method}_n{n}")
-        except Exception:
-            traffic = None
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": kname, "kernel_ms": ms_kernel, "peak_source": peak_src,
-                "frac_of_nominal_8TBs": achieved / NOMINAL_HBM_GBS,
-                "frac_of_measured_read_ceiling_7400": achieved / 7400.0,
-                "algorithmic_bytes_per_launch": 8.0 * m * n}
+    ms_kernel = rig.max_ranks(sum(a.elapsed_time(b) for a, b in pairs) / len(pairs))
+    bound, t_floor, flops = roofline_bound("tsqr" if args.method == "tsqr" else "gram", m, n, peak)
+    achieved_gbs = 8.0 * m * n / (ms_kernel * 1e-3) / 1e9
+    if bound == "hbm":
+        roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
+                    "frac": achieved_gbs / peak, "peak_source": peak_src}
+    else:  # FP64 pipe (DFMA and DMMA share it): algorithmic flops of the pass against the measured FP64 peak
+        ach = flops / (ms_kernel * 1e-3) / 1e12
+        roofline = {"bound": "fp64", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": ach / FP64_PEAK_TFLOPS,
+                    "peak_source": "measured FP64 DFMA/DMMA peak at 1.965 GHz (profiles/probes/probe_fp64.txt); "
+                                   "the HBM roofline is not the binding one at this column count",
+                    "achieved_gbs": achieved_gbs, "frac_of_hbm_copy_peak": achieved_gbs / peak}
+    roofline.update({"traffic": traffic_per_launch(args.method, n, m), "kernel": kname, "kernel_ms": ms_kernel,
+                     "frac_of_nominal_8TBs": achieved_gbs / NOMINAL_HBM_GBS,
+                     "frac_of_measured_read_ceiling": achieved_gbs / READ_CEILING_GBS,
+                     "algorithmic_bytes_per_launch": 8.0 * m * n, "algorithmic_flops_per_launch": flops,
+                     "binding_floor_ms": t_floor * 1e3, "timed_on": "settled board (burst clocks)"})
 
+    # ---- headline: the same K steps after 300 ms of back-to-back steps (sustained, on the power cap) --
     time.sleep(0.5)
-    # the same K steps after 300 ms of back-to-back steps: the sustained figure under the power cap
     sampler2 = ClockSampler(local)
     sampler2.start()
-    ms_sus, _ = timed(lambda: run_method(x, args.method), args.steps, args.warmup, spinup_ms=300.0)
-    clocks_sus = sampler2.stop()
-    sustained = {"value": total_bytes / (ms_sus * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms_sus,
-                 "clocks": clocks_sus, "note": "same K steps after 300 ms of untimed back-to-back steps"}
+    ms_step, launches = rig.timed(lambda: run_method(x, args.method), args.steps, args.warmup, spinup_ms=300.0)
+    clocks = sampler2.stop()
+    value = total_bytes / (ms_step * 1e-3) / 1e9
 
     out = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.method} m=2^27 n={n} Gaussian (BASELINE configs[1], headline point "
-                               f"of the column sweep)", "m_per_gpu": m, "n": n, "method": args.method,
+        "config": {"workload": f"{args.method} m=2^27 n={n} Gaussian (BASELINE configs[1], headline point of the "
+                               f"column sweep); value = SUSTAINED (K steps after 300 ms of untimed back-to-back "
+                               f"steps, board on its power cap), burst = the same K steps on a settled board",
+                   "m_per_gpu": m, "n": n, "method": args.method,
                    "l2": "inputs (>= 1 GiB) larger than the 126 MB L2; no flush needed",
-                   "plan": {"num_blocks": plan.num_blocks, "panel_rows": plan.panel_rows}},
-        "clocks": clocks, "gpu_launches": launches, "roofline": roofline, "sustained": sustained,
+                   "plan": {"num_blocks": plan.num_blocks, "panel_rows": plan.panel_rows},
+                   "transport": rig.transport},
+        "clocks": clocks, "gpu_launches": launches, "roofline": roofline,
+        "burst": {"value": burst, "unit": "GB/s", "ms_per_step": ms_burst, "clocks": clocks_burst,
+                  "frac_of_nominal_8TBs": burst / (NOMINAL_HBM_GBS * world)},
         "frac_of_nominal_8TBs": value / (NOMINAL_HBM_GBS * world),
     }
 
@@ -319,22 +389,23 @@ def main():
         xh_t = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
         xh_t.copy_(x.t())
         xh = xh_t.numpy().T  # F-ordered m x n view of pinned memory
-        fn = {"tsqr": ctx.tsqr_qless, "cholqr2": ctx.cholqr2, "svqb2": ctx.svqb2}[args.method]
-        e2e_steps = max(3, min(args.steps, 10))
-        fn(xh)
-        sync_all()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            r_host = fn(xh)
-        sync_all()
-        dt = (time.perf_counter() - t0) / e2e_steps
-        if dist is not None:
-            t = torch.tensor([dt], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
-        out["e2e"] = {"value": total_bytes / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 8 * m * n,
-                      "d2h_bytes_per_step": 8 * n * n, "ms_per_step": dt * 1e3, "steps": e2e_steps,
-                      "api": f"paper_2603_20889_b200.{fn.__name__}(numpy pinned host array) -> sqb_*_host"}
+        if world > 1:
+            fn = {"tsqr": ctx.tsqr_qless_sharded_host}.get(args.method)
+        else:
+            fn = {"tsqr": ctx.tsqr_qless, "cholqr2": ctx.cholqr2, "svqb2": ctx.svqb2}[args.method]
+        if fn is not None:
+            e2e_steps = max(3, min(args.steps, 10))
+            fn(xh)
+            rig.sync_all()
+            t0 = time.perf_counter()
+            for _ in range(e2e_steps):
+                fn(xh)
+            rig.sync_all()
+            dt = rig.max_ranks((time.perf_counter() - t0) / e2e_steps)
+            out["e2e"] = {"value": total_bytes / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 8 * m * n,
+                          "d2h_bytes_per_step": 8 * n * n, "ms_per_step": dt * 1e3, "steps": e2e_steps,
+                          "api": f"paper_2603_20889_b200.{fn.__name__}(numpy pinned host array) -> sqb_*_host "
+                                 f"(X streamed through a 3-slab ring, {ctx.host_slab_bytes >> 20} MiB slabs)"}
         del xh, xh_t
 
     # ---- the reference's CPU path on this box's host cores, bounded sample --------------------------
@@ -342,7 +413,7 @@ def main():
         try:
             mc = args.cpu_rows or (1 << 27) // max(n, 8)
             xs = np.asfortranarray(x[:mc].cpu().numpy())
-            best, mean, info = cpu_reference_run(mc, n, 5, 1, args.method if args.method != "svqb2" else "svqb2", xs)
+            best, mean, info = cpu_reference_run(mc, n, 5, 1, args.method, xs)
             info.update({"value": mean, "unit": "GB/s", "best": best})
             out["cpu_baseline"] = info
             # parity of the headline run against the reference on that sample
@@ -350,10 +421,11 @@ def main():
             r_gpu = run_method(x[:mc], args.method)
             ctx.synchronize()
             if args.method != "svqb2":
-                r_cpu = (oracle.ref or oracle.port).tsqr_qless(xs) if args.method == "tsqr" else (oracle.ref or oracle.port).cholqr2(xs)
+                o = oracle.ref or oracle.port
+                r_cpu = o.tsqr_qless(xs) if args.method == "tsqr" else o.cholqr2(xs)
                 err = float(np.linalg.norm(r_gpu.cpu().numpy() - r_cpu))
                 out["parity"] = {"abs_err_F": err, "bound_64_n_eps_normX": float(64 * n * 2.22e-16 * np.linalg.norm(xs)),
-                                 "rows": mc}
+                                 "rows": mc, "oracle": "reference" if oracle.ref else "port"}
         except Exception as exc:  # the baseline must never sink the bench line
             out["cpu_baseline"] = {"error": repr(exc)}
 
@@ -367,16 +439,20 @@ def main():
         hw.mem_bandwidth = peak * 1e9
         out["model_hardware"] = {"name": hw.name, "mem_bandwidth": hw.mem_bandwidth, "peak_fp64": hw.peak_fp64,
                                  "machine_balance": pmod.machine_balance(hw)}
+        out["sweep_protocol"] = f"{args.sweep_reps} timed reps after 3 warm-ups per point (reference PAPER.md:305-307)"
         sweep = []
         for nn in (1, 2, 4, 8, 16, 32, 64):
             xs = ctx.fill_gaussian(m, nn, seed=1234)
             row = {"n": nn, "gib": 8.0 * m * nn / 2**30}
             for meth in ("tsqr", "cholqr2", "svqb2"):
                 try:
-                    ms, _ = timed(lambda: run_method(xs, meth), args.sweep_reps, 2)
+                    ms, _ = rig.timed(lambda: run_method(xs, meth), args.sweep_reps, 3)
                     gbs = 8.0 * m * nn / (ms * 1e-3) / 1e9
                     model_s = pmod.composite_time(hw, meth, m, nn)
+                    bnd, t_fl, _ = roofline_bound("tsqr" if meth == "tsqr" else "gram", m, nn, peak)
+                    passes = 1 if meth == "tsqr" else 2
                     row[meth] = {"ms": ms, "gbs": gbs, "frac_8TBs": gbs / NOMINAL_HBM_GBS, "frac_measured": gbs / peak,
+                                 "bound": bnd, "frac_of_binding_roofline": passes * t_fl * 1e3 / ms,
                                  "model_time_s": model_s, "model_ratio": ms * 1e-3 / model_s}
                     if meth == "tsqr":
                         row[meth]["fp64_tflops_2mn2"] = 2.0 * m * nn * nn / (ms * 1e-3) / 1e12
@@ -386,11 +462,109 @@ def main():
             del xs
             torch.cuda.empty_cache()
         out["sweep"] = sweep
+    return out
 
-    if rank == 0:
+
+def run_c4(rig, args):
+    """BASELINE configs[3]: single-pass least squares via Q-less QR of [A b], 1e9 x 16 FP64 (A: 15
+    columns + b), rows sharded over the ranks (strong scaling: the total row count is fixed), n x n
+    combine over NCCL.  The right-hand side is b = A x_true + 1e-3 * noise, so the solution is known."""
+    import numpy as np
+    torch, ctx = rig.torch, rig.ctx
+    rank, world = rig.rank, rig.world
+    m_total, ncols = args.c4_rows, 16
+    n = ncols - 1
+    lo, hi = rig.sharding.slab_bounds(m_total, world, rank)
+    ml = hi - lo
+    xl = ctx.fill_gaussian(ml, ncols, seed=1234, row_offset=lo, m_total=m_total)  # [A noise]
+    a, rhs = xl[:, :n], xl[:, n]
+    x_true = torch.linspace(-1.0, 1.0, n, dtype=torch.float64, device=rig.dev)
+    rhs.mul_(1e-3)
+    for j in range(n):  # harness only: b = A x_true + 1e-3 noise, one column at a time (no m x n temporary)
+        rhs.add_(a[:, j], alpha=float(x_true[j]))
+    torch.cuda.synchronize()
+    time.sleep(1.0)
+
+    def step():
+        return ctx.solve_lstsq_sharded(a, rhs) if world > 1 else ctx.solve_lstsq(a, rhs, "tsqr")
+
+    sampler = ClockSampler(rig.local)
+    sampler.start()
+    ms_step, launches = rig.timed(step, args.steps, args.warmup, spinup_ms=300.0)
+    clocks = sampler.stop()
+    xs, res = step()
+    ctx.synchronize("c4")
+    xs_h = xs.cpu().numpy()
+    err = float(np.max(np.abs(xs_h - x_true.cpu().numpy())))
+    # every rank must hold the same bits
+    same = True
+    if rig.dist is not None:
+        ref = xs.clone()
+        rig.dist.broadcast(ref, src=0)
+        same = bool(torch.equal(ref, xs))
+        flag = torch.tensor([1.0 if same else 0.0], device=rig.dev, dtype=torch.float64)
+        rig.dist.all_reduce(flag, op=rig.dist.ReduceOp.MIN)
+        same = bool(flag.item() == 1.0)
+    total_bytes = 8.0 * m_total * ncols
+    value = total_bytes / (ms_step * 1e-3) / 1e9
+    peak, peak_src = measured_peaks()
+    return {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"solve_lstsq via Q-less TSQR of [A b], {m_total} x {ncols} FP64 (A {n} columns + b), "
+                               f"rows sharded over {world} GPU(s) (BASELINE configs[3]); sustained (300 ms spin-up)",
+                   "m_total": m_total, "rows_per_gpu": ml, "n": n, "transport": rig.transport,
+                   "l2": "slab (>= 16 GB per GPU) larger than the 126 MB L2"},
+        "clocks": clocks, "gpu_launches": launches,
+        "solution": {"max_abs_err_vs_x_true": err, "noise_over_sqrt_m": 1e-3 / np.sqrt(m_total),
+                     "residual": float(res.item()), "identical_on_all_ranks": same},
+        "roofline": {"bound": "hbm" if ncols <= 12 else "fp64", "achieved": value / world, "peak": peak, "unit": "GB/s",
+                     "frac": value / world / peak, "traffic": None, "peak_source": peak_src,
+                     "note": "whole step per GPU (streaming kernel + combine + exchange) against the copy bandwidth; "
+                             "16 columns is past the HBM-bound range of the Householder kernels (FP64 floor "
+                             f"{2.0 * ml * ncols * ncols / (FP64_PEAK_TFLOPS * 1e12) * 1e3:.2f} ms per GPU)"},
+        "frac_of_nominal_8TBs": value / (NOMINAL_HBM_GBS * world),
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="sweep", choices=["sweep", "c4"])
+    ap.add_argument("--n", type=int, default=8, help="columns of the headline workload")
+    ap.add_argument("--m", type=int, default=1 << 27, help="rows per GPU")
+    ap.add_argument("--c4-rows", type=int, default=10**9, help="total rows of the c4 least-squares problem")
+    ap.add_argument("--method", default="tsqr", choices=["tsqr", "cholqr2", "svqb2"])
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sweep-reps", type=int, default=50)
+    ap.add_argument("--cpu-rows", type=int, default=0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # no launcher around us: start one process per GPU ourselves
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible")
+        return sys.exit(subprocess.call(spawn_command(args.gpus, sys.argv[1:], free_port())))
+
+    rig = Rig()
+    if rig.world != args.gpus and rig.rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but the launcher started {rig.world} rank(s); reporting n_gpus = "
+              f"{rig.world}", file=sys.stderr)
+    out = run_c4(rig, args) if args.config == "c4" else run_headline(rig, args)
+    if rig.rank == 0:
         print(json.dumps(out))
-    if dist is not None:
-        dist.destroy_process_group()
+    rig.close()
 
 
 if __name__ == "__main__":

@@ -65,6 +65,19 @@ int sqb_device_sm_count(const sqb_context* ctx);
 /* Number of kernels launched through this context since creation (bench bookkeeping).      */
 long long sqb_launch_count(const sqb_context* ctx);
 
+/* Test / tuning hook: force one TSQR kernel family for this context (0 = thread-private leaves,
+ * 1 = lookahead fold, 2 = FP64 tensor-core blocked kernel, -1 = the measured selection table).
+ * A family that cannot run a given column count falls back to the table.                     */
+int sqb_set_tsqr_kernel(sqb_context* ctx, int kind);
+/* Slab size (bytes, >= 1 MiB) of the host-pointer entry points: single-pass calls stream X
+ * through a three-slab ring, so device memory stays O(slab) however large m*n is (the reference
+ * keeps O((b+n)*n) state, src/tsqr.cpp:143-147).                                              */
+int sqb_set_host_slab_bytes(sqb_context* ctx, int64_t bytes);
+/* Stream-ordered copies between host memory and device buffers of this context's device; both
+ * synchronise the stream before returning (used by caller-supplied exchanges, below).         */
+int sqb_copy_h2d(sqb_context* ctx, void* d_dst, const void* h_src, int64_t bytes);
+int sqb_copy_d2h(sqb_context* ctx, void* h_dst, const void* d_src, int64_t bytes);
+
 /* ---- plans (replaces default_tsqr_plan / default_gram_plan, src/plan.cpp:9-32) ---------- */
 /* num_blocks = CTAs of the streaming kernel (reference: worker threads), panel_rows = rows
  * one warp stages per TMA transaction group (reference: cache-resident panel height).       */
@@ -170,7 +183,32 @@ int sqb_fill_gaussian_dev(sqb_context* ctx, double* d_x, int64_t m, int64_t n, i
 int sqb_generate_dev(sqb_context* ctx, double* d_x, int64_t m, int64_t n, int64_t ld,
                      double kappa, int linear_decay, uint64_t seed);
 
-/* ---- multi-GPU (one process per GPU; rows sharded, only n x n data crosses NVLink) ---------- */
+/* ---- multi-GPU (one process per GPU; rows sharded, only n x n data crosses NVLink) ----------
+ * The protocol is the reference's own block structure one level up: rank g plays the part of
+ * block g.  TSQR: every rank reduces its slab to an n x n triangle, the triangles are all-gathered
+ * and every rank runs stage 2 over the (world*n) x n stack (src/tsqr.cpp:175-195 with k = world).
+ * Gram methods: every rank forms its partial n x n Gram, the partials are all-gathered and summed
+ * in ascending rank order (src/gram.cpp:81-92), so all ranks hold bit-identical matrices.  The
+ * exchange is NCCL (sqb_init_nccl / sqb_attach_nccl) or any caller-supplied all-gather
+ * (sqb_set_allgather: MPI, torch.distributed, a test harness) - the same driver code runs over
+ * either.  The two halves are also exported on their own (sqb_tsqr_local_dev + sqb_*_combine_dev).   */
+/* All-gather of `count` doubles per rank: d_send (this rank's block) -> d_recv (world blocks in
+ * rank order), both device pointers on the context's device.  It is called between kernel
+ * launches on the context's stream (sqb_get_stream); d_send is ready in stream order and d_recv
+ * must be valid for work enqueued on that stream afterwards.  Return 0 on success.               */
+typedef int (*sqb_allgather_fn)(void* user, const double* d_send, double* d_recv, int64_t count);
+int sqb_set_allgather(sqb_context* ctx, sqb_allgather_fn fn, void* user, int rank, int world);
+/* This rank's triangle: Q-less TSQR of its slab WITHOUT sign normalisation (block_qless_qr of
+ * block `rank`, src/tsqr.cpp:178-181); m_local may be smaller than n or zero (zero triangle).    */
+int sqb_tsqr_local_dev(sqb_context* ctx, const double* d_x, int64_t m_local, int64_t n, int64_t ld,
+                       double* d_r_local);
+/* Stage 2 over `world` gathered triangles (d_gathered: world blocks of n x n, leading dimension
+ * n): stack, fold, sign-normalise (src/tsqr.cpp:193-195, src/types.cpp:8-14).                     */
+int sqb_tsqr_combine_dev(sqb_context* ctx, const double* d_gathered, int64_t world, int64_t n,
+                         double* d_r);
+/* Sum of `world` gathered n x n Gram partials in ascending rank order (src/gram.cpp:81-92).      */
+int sqb_gram_combine_dev(sqb_context* ctx, const double* d_gathered, int64_t world, int64_t n,
+                         double* d_c);
 /* Attach an ncclComm_t created by the caller (e.g. from torch.distributed's unique id).      */
 int sqb_attach_nccl(sqb_context* ctx, void* nccl_comm, int rank, int world);
 /* Create a communicator from a 128-byte ncclUniqueId (all ranks call collectively).          */
@@ -181,6 +219,9 @@ int sqb_init_nccl(sqb_context* ctx, const void* unique_id128, int rank, int worl
  * CholQR2/SVQB2: all-reduce of each n x n Gram.                                              */
 int sqb_tsqr_qless_sharded_dev(sqb_context* ctx, const double* d_x, int64_t m_local, int64_t n,
                                int64_t ld, double* d_r);
+/* Host-pointer form: this rank's slab lives in host memory and streams through the slab ring.  */
+int sqb_tsqr_qless_sharded_host(sqb_context* ctx, const double* x, int64_t m_local, int64_t n,
+                                int64_t ld, double* r);
 int sqb_cholqr2_sharded_dev(sqb_context* ctx, const double* d_x, int64_t m_local, int64_t n,
                             int64_t ld, double* d_r);
 int sqb_svqb2_sharded_dev(sqb_context* ctx, const double* d_x, int64_t m_local, int64_t n,

@@ -42,6 +42,9 @@ LIB_NAME = "libskinnyqr_b200.so"
 
 I64 = C.c_int64
 DP = C.POINTER(C.c_double)
+# sqb_allgather_fn (include/skinnyqr_b200.h): user, d_send, d_recv, count -> status
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64)
+TSQR_KERNELS = {"auto": -1, "thread": 0, "fold": 1, "mma": 2}
 
 
 # ---- exception hierarchy (reference include/skinnyqr/types.hpp:11-77) -------------------------
@@ -118,6 +121,7 @@ class PanelPlan:
 # ---- library loading ---------------------------------------------------------------------------
 ABI_SYMBOLS = [
     "sqb_create", "sqb_destroy", "sqb_set_stream", "sqb_use_own_stream", "sqb_get_stream", "sqb_sync",
+    "sqb_set_tsqr_kernel", "sqb_set_host_slab_bytes", "sqb_copy_h2d", "sqb_copy_d2h",
     "sqb_last_error_index", "sqb_status_string", "sqb_device_sm_count", "sqb_launch_count",
     "sqb_default_tsqr_plan", "sqb_default_gram_plan",
     "sqb_tsqr_qless_dev", "sqb_tsqr_stage1_dev", "sqb_block_qless_qr_dev", "sqb_tsmttsm_dev",
@@ -129,7 +133,8 @@ ABI_SYMBOLS = [
     "sqb_cholqr2_host", "sqb_svqb_pass_host", "sqb_svqb2_host", "sqb_reconstruct_q_host",
     "sqb_solve_lstsq_host",
     "sqb_fill_gaussian_dev", "sqb_generate_dev",
-    "sqb_attach_nccl", "sqb_nccl_unique_id", "sqb_init_nccl", "sqb_tsqr_qless_sharded_dev",
+    "sqb_attach_nccl", "sqb_nccl_unique_id", "sqb_init_nccl", "sqb_set_allgather", "sqb_tsqr_local_dev",
+    "sqb_tsqr_combine_dev", "sqb_gram_combine_dev", "sqb_tsqr_qless_sharded_dev", "sqb_tsqr_qless_sharded_host",
     "sqb_cholqr2_sharded_dev", "sqb_svqb2_sharded_dev", "sqb_solve_lstsq_sharded_dev",
 ]
 
@@ -216,6 +221,7 @@ class Context:
             self.handle = None
             _raise(st, -1, "sqb_create")
         self.device = device
+        self.host_slab_bytes = 256 << 20
         self._torch_stream = -1  # cudaStream_t of torch's current stream once device tensors are used
 
     def close(self):
@@ -289,6 +295,38 @@ class Context:
             raise ArgumentError("device matrices must be column-major (stride (1, ld))")
         return C.c_void_p(t.data_ptr()), m, n, (s1 if n > 1 else max(m, 1))
 
+    def _dev_square(self, t, n, what):
+        """A secondary n x n device operand (R, B, C): float64, same device, packed column-major."""
+        p, fm, fn_, fld = self._dev(t)
+        if t.dim() != 2 or (fm, fn_) != (n, n):
+            raise DimensionError(f"{what} must be n x n")
+        if fld != n:
+            raise ArgumentError(f"{what} must be a packed column-major n x n matrix (leading dimension n)")
+        if t.device.index != self.device:
+            raise ArgumentError(f"{what} lives on another device")
+        return p
+
+    def _dev_vector(self, t, m, what):
+        """A device vector operand (rhs): float64, same device, unit stride, m entries."""
+        import torch
+        if not _is_torch(t) or t.dtype != torch.float64 or not t.is_cuda:
+            raise ArgumentError(f"{what} must be a float64 CUDA tensor")
+        if t.dim() != 1 or t.shape[0] != m:
+            raise DimensionError(f"{what} must have {m} entries")
+        if m > 1 and t.stride(0) != 1:
+            raise ArgumentError(f"{what} must have unit stride")
+        if t.device.index != self.device:
+            raise ArgumentError(f"{what} lives on another device")
+        return C.c_void_p(t.data_ptr())
+
+    def set_tsqr_kernel(self, kind="auto"):
+        """Force one TSQR kernel family ("thread", "fold", "mma") or return to the table ("auto")."""
+        self._check(self.lib.sqb_set_tsqr_kernel(self.handle, C.c_int(TSQR_KERNELS[kind])), "set_tsqr_kernel")
+
+    def set_host_slab_bytes(self, nbytes):
+        self._check(self.lib.sqb_set_host_slab_bytes(self.handle, I64(int(nbytes))), "set_host_slab_bytes")
+        self.host_slab_bytes = int(nbytes)
+
     def empty_matrix(self, m, n):
         """Column-major m x n float64 CUDA tensor (shape (m, n), stride (1, m))."""
         import torch
@@ -358,9 +396,7 @@ class Context:
             if factor is None:
                 st = fn(self.handle, p, I64(m), I64(n), I64(ld), I64(k), I64(b), self._ptr(c))
             else:
-                fp, fm, fn_, fld = self._dev(factor)
-                if (fm, fn_) != (n, n) or fld != n:
-                    raise DimensionError(f"{name}: factor must be a packed n x n matrix")
+                fp = self._dev_square(factor, n, f"{name}: factor")
                 st = fn(self.handle, p, I64(m), I64(n), I64(ld), fp, I64(k), I64(b), self._ptr(c))
             self._check(st, name)
             return c
@@ -390,7 +426,10 @@ class Context:
     # -- n x n factorisations and Gram-based drivers (gram_qr.hpp:37-59)
     def cholesky(self, c):
         if _is_torch(c):
-            p, n, n2, ld = self._dev(c)
+            if c.dim() != 2 or c.shape[0] != c.shape[1]:
+                raise DimensionError("cholesky: C must be square")
+            n = c.shape[0]
+            p = self._dev_square(c, n, "cholesky: C")
             r = self._square(n)
             self._check(self.lib.sqb_cholesky_dev(self.handle, p, I64(n), self._ptr(r)), "cholesky")
             return r
@@ -454,7 +493,7 @@ class Context:
     def reconstruct_q(self, x, r):
         if _is_torch(x):
             p, m, n, ld = self._dev(x)
-            rp, _, _, _ = self._dev(r)
+            rp = self._dev_square(r, n, "reconstruct_q: R")
             q = self.empty_matrix(m, n)
             self._check(self.lib.sqb_reconstruct_q_dev(self.handle, p, I64(m), I64(n), I64(ld), rp,
                                                        self._ptr(q), I64(m)), "reconstruct_q")
@@ -474,11 +513,10 @@ class Context:
         if _is_torch(a):
             import torch
             p, m, n, ld = self._dev(a)
-            if rhs.shape[0] != m:
-                raise DimensionError("solve_lstsq: rhs length != rows of A")
+            rp = self._dev_vector(rhs, m, "solve_lstsq: rhs")
             x = torch.empty(n, dtype=torch.float64, device=a.device)
             res = torch.empty(1, dtype=torch.float64, device=a.device)
-            self._check(self.lib.sqb_solve_lstsq_dev(self.handle, p, I64(m), I64(n), I64(ld), self._ptr(rhs),
+            self._check(self.lib.sqb_solve_lstsq_dev(self.handle, p, I64(m), I64(n), I64(ld), rp,
                                                      C.c_int(meth), self._ptr(x), self._ptr(res)),
                         "solve_lstsq")
             return x, res
@@ -518,11 +556,79 @@ class Context:
         self._check(self.lib.sqb_init_nccl(self.handle, C.c_char_p(unique_id), C.c_int(rank), C.c_int(world)),
                     "init_nccl")
 
+    def set_allgather(self, gather, rank: int, world: int):
+        """Route the n x n exchange of the sharded drivers through `gather(d_send, d_recv, count)`
+        (integer device addresses; return 0 on success) instead of NCCL - see sharding.TorchExchange."""
+        def _cb(_user, send, recv, count):
+            try:
+                return int(gather(send, recv, int(count)) or 0)
+            except Exception:  # an exception must not unwind through the C frames
+                import traceback
+                traceback.print_exc()
+                return 1
+        self._gather_cb = ALLGATHER_FN(_cb)  # keep the thunk alive as long as the context uses it
+        self._check(self.lib.sqb_set_allgather(self.handle, self._gather_cb, None, C.c_int(rank), C.c_int(world)),
+                    "set_allgather")
+
+    def copy_d2h(self, host_array, dev_ptr):
+        self._check(self.lib.sqb_copy_d2h(self.handle, host_array.ctypes.data_as(C.c_void_p), C.c_void_p(dev_ptr),
+                                          I64(host_array.nbytes)), "copy_d2h")
+
+    def copy_h2d(self, dev_ptr, host_array):
+        self._check(self.lib.sqb_copy_h2d(self.handle, C.c_void_p(dev_ptr), host_array.ctypes.data_as(C.c_void_p),
+                                          I64(host_array.nbytes)), "copy_h2d")
+
+    def tsqr_local(self, x):
+        """This rank's un-normalised triangle (first half of the sharded TSQR)."""
+        p, m, n, ld = self._dev(x)
+        r = self._square(n)
+        self._check(self.lib.sqb_tsqr_local_dev(self.handle, p, I64(m), I64(n), I64(ld), self._ptr(r)), "tsqr_local")
+        return r
+
+    def _gathered(self, blocks, what):
+        """(world, n, n) stack of column-major n x n blocks -> contiguous device buffer."""
+        import torch
+        if _is_torch(blocks):
+            g = blocks
+        else:
+            g = torch.stack([b.t().contiguous() for b in blocks])  # each block column-major in memory
+        if g.dim() != 3 or g.shape[1] != g.shape[2] or not g.is_contiguous():
+            raise DimensionError(f"{what}: expected world contiguous n x n blocks")
+        if g.dtype != torch.float64 or not g.is_cuda or g.device.index != self.device:
+            raise ArgumentError(f"{what}: blocks must be float64 CUDA tensors on this device")
+        self._dev(g[0])  # stream bookkeeping
+        return g, g.shape[0], g.shape[1]
+
+    def tsqr_combine(self, blocks):
+        """Stage 2 over gathered triangles (list of n x n device tensors in rank order)."""
+        g, world, n = self._gathered(blocks, "tsqr_combine")
+        r = self._square(n)
+        self._check(self.lib.sqb_tsqr_combine_dev(self.handle, self._ptr(g), I64(world), I64(n), self._ptr(r)),
+                    "tsqr_combine")
+        return r
+
+    def gram_combine(self, blocks):
+        """Sum of gathered Gram partials in ascending rank order."""
+        g, world, n = self._gathered(blocks, "gram_combine")
+        c = self._square(n)
+        self._check(self.lib.sqb_gram_combine_dev(self.handle, self._ptr(g), I64(world), I64(n), self._ptr(c)),
+                    "gram_combine")
+        return c
+
     def tsqr_qless_sharded(self, x):
         p, m, n, ld = self._dev(x)
         r = self._square(n)
         self._check(self.lib.sqb_tsqr_qless_sharded_dev(self.handle, p, I64(m), I64(n), I64(ld), self._ptr(r)),
                     "tsqr_qless_sharded")
+        return r
+
+    def tsqr_qless_sharded_host(self, x):
+        """Host slab of this rank in, host R out (slab ring + exchange)."""
+        x = _fmat(x)
+        m, n = x.shape
+        r = np.zeros((n, n), order="F")
+        self._check(self.lib.sqb_tsqr_qless_sharded_host(self.handle, _hp(x), I64(m), I64(n), I64(m), _hp(r)),
+                    "tsqr_qless_sharded_host")
         return r
 
     def cholqr2_sharded(self, x):
@@ -546,10 +652,11 @@ class Context:
     def solve_lstsq_sharded(self, a, rhs):
         import torch
         p, m, n, ld = self._dev(a)
+        rp = self._dev_vector(rhs, m, "solve_lstsq_sharded: rhs")
         x = torch.empty(n, dtype=torch.float64, device=a.device)
         res = torch.empty(1, dtype=torch.float64, device=a.device)
         self._check(self.lib.sqb_solve_lstsq_sharded_dev(self.handle, p, I64(m), I64(n), I64(ld),
-                                                         self._ptr(rhs), self._ptr(x), self._ptr(res)),
+                                                         rp, self._ptr(x), self._ptr(res)),
                     "solve_lstsq_sharded")
         return x, res
 
@@ -571,6 +678,18 @@ def _ctx_for(x):
     return default_context(0)
 
 
+def _call(x, name, args, check):
+    """Module-level entry: host arrays are synchronous anyway; for device tensors `check=True`
+    (the default) synchronises and raises the reference's exception for a numerical failure right
+    here - with check=False the call stays asynchronous and failures surface at the next
+    Context.synchronize()."""
+    ctx = _ctx_for(x)
+    out = getattr(ctx, name)(*args)
+    if check and _is_torch(x):
+        ctx.synchronize(name)
+    return out
+
+
 def sign_normalize(r):
     """reference types.cpp:8-14 (host n x n helper): negate row i from the diagonal on when
     R(i,i) < 0."""
@@ -589,53 +708,53 @@ def default_gram_plan(m, n):
     return default_context().default_gram_plan(m, n)
 
 
-def tsqr_qless(x, plan=None):
-    return _ctx_for(x).tsqr_qless(x, plan)
+def tsqr_qless(x, plan=None, check=True):
+    return _call(x, "tsqr_qless", (x, plan), check)
 
 
-def tsqr_stage1(x, plan=None):
-    return _ctx_for(x).tsqr_stage1(x, plan)
+def tsqr_stage1(x, plan=None, check=True):
+    return _call(x, "tsqr_stage1", (x, plan), check)
 
 
-def block_qless_qr(x, b=0):
-    return _ctx_for(x).block_qless_qr(x, b)
+def block_qless_qr(x, b=0, check=True):
+    return _call(x, "block_qless_qr", (x, b), check)
 
 
-def tsmttsm(x, plan=None):
-    return _ctx_for(x).tsmttsm(x, plan)
+def tsmttsm(x, plan=None, check=True):
+    return _call(x, "tsmttsm", (x, plan), check)
 
 
-def tsmRttsmR(x, r, plan=None):
-    return _ctx_for(x).tsmRttsmR(x, r, plan)
+def tsmRttsmR(x, r, plan=None, check=True):
+    return _call(x, "tsmRttsmR", (x, r, plan), check)
 
 
-def tsmmttsmm(x, b, plan=None):
-    return _ctx_for(x).tsmmttsmm(x, b, plan)
+def tsmmttsmm(x, b, plan=None, check=True):
+    return _call(x, "tsmmttsmm", (x, b, plan), check)
 
 
-def cholesky(c):
-    return _ctx_for(c).cholesky(c)
+def cholesky(c, check=True):
+    return _call(c, "cholesky", (c,), check)
 
 
 def eigh_small(c):
     return default_context().eigh_small(c)
 
 
-def cholqr2(x, plan=None):
-    return _ctx_for(x).cholqr2(x, plan)
+def cholqr2(x, plan=None, check=True):
+    return _call(x, "cholqr2", (x, plan), check)
 
 
 def svqb_pass(c):
     return default_context().svqb_pass(c)
 
 
-def svqb2(x, plan=None):
-    return _ctx_for(x).svqb2(x, plan)
+def svqb2(x, plan=None, check=True):
+    return _call(x, "svqb2", (x, plan), check)
 
 
-def reconstruct_q(x, r):
-    return _ctx_for(x).reconstruct_q(x, r)
+def reconstruct_q(x, r, check=True):
+    return _call(x, "reconstruct_q", (x, r), check)
 
 
-def solve_lstsq(a, rhs, method="tsqr"):
-    return _ctx_for(a).solve_lstsq(a, rhs, method)
+def solve_lstsq(a, rhs, method="tsqr", check=True):
+    return _call(a, "solve_lstsq", (a, rhs, method), check)

@@ -16,11 +16,11 @@ CSRC = PKG / "csrc"
 OUT = PKG / "libskinnyqr_b200.so"
 OBJ = PKG / "build"
 INCLUDE = PKG.parent / "include"
-SOURCES = ["tsqr_kernels.cu", "tsqr_thread_kernels.cu", "tsqr_group_kernels.cu", "tsqr_fold_kernels.cu", "tsqr_mma_kernels.cu", "gram_kernels.cu", "gram_wide_kernels.cu", "gram_thread_kernels.cu", "small_kernels.cu", "matgen_kernels.cu", "capi.cu"]
+SOURCES = ["tsqr_thread_kernels.cu", "tsqr_fold_kernels.cu", "tsqr_mma_kernels.cu", "gram_kernels.cu", "gram_wide_kernels.cu", "gram_thread_kernels.cu", "small_kernels.cu", "matgen_kernels.cu", "capi.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
     "-Xcompiler", "-fPIC", "-I", str(INCLUDE), "-I", str(CSRC),
-] + (["-DSQB_FOLD_EXPERIMENT"] if os.environ.get("SQB_FOLD_EXPERIMENT") else [])  # extra (NS, G, P) variants for tuning
+]
 
 
 def _nvcc() -> str:

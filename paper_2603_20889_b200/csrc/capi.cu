@@ -60,7 +60,7 @@ Plan make_plan(long long m, long long k, long long b) {
 // B200 default for the Householder stream: one CTA per SM (the kernel owns the whole shared
 // memory), b = the warp panel height; fewer CTAs when there is not even one panel per warp.
 Plan tsqr_plan(const sqb_context* ctx, long long m, int n, long long k, long long b) {
-  const long long P = tsqr_panel_rows(n), NW = tsqr_warps(n);
+  const long long P = tsqr_panel_rows(n, ctx->tsqr_kind), NW = tsqr_warps(n, ctx->tsqr_kind);
   if (b <= 0) b = P;
   if (k <= 0) k = std::max<long long>(1, std::min<long long>(ctx->sm_count, m / (P * NW)));
   return make_plan(m, k, b);
@@ -96,6 +96,7 @@ int launch_tsqr(sqb_context* ctx, const MatView& v, long long m, int n, const Pl
   prm.finalize = finalize ? 1 : 0;
   prm.check_finite = check ? 1 : 0;
   prm.status = ctx->d_status;
+  prm.kind = ctx->tsqr_kind;
   SQB_CUDA(launch_tsqr_any(prm, p.k, ctx->stream));
   ctx->launches++;
   return SQB_OK;
@@ -105,7 +106,7 @@ int launch_tsqr(sqb_context* ctx, const MatView& v, long long m, int n, const Pl
 // triangle: the reference's stage 2 (tsqr.cpp:193-195), as a short tree of the same kernel.
 int reduce_stack(sqb_context* ctx, double* stack, long long rows, long long ld, int n,
                  double* scratch, double* d_r, bool finalize) {
-  const long long P = tsqr_panel_rows(n), NW = tsqr_warps(n);
+  const long long P = tsqr_panel_rows(n, ctx->tsqr_kind), NW = tsqr_warps(n, ctx->tsqr_kind);
   double* cur = stack;
   double* nxt = scratch;
   while (true) {
@@ -287,23 +288,73 @@ int translate_status(sqb_context* ctx) {
 }
 
 // ---- host-pointer plumbing -------------------------------------------------------------------
-// Streams X into a resident device buffer in row slabs (copy stream) and hands every slab, as soon
-// as it has landed, to `on_slab(row0, rows)` which enqueues work on the compute stream.
-constexpr size_t kSlabBytes = 256u << 20;
+// Two ways to bring a host matrix to the GPU.
+//  * upload_resident: the whole matrix lands in ctx->xbuf (leading dimension rounded up to an even
+//    row count so that every column stays 16-byte aligned whatever the parity of m) - for the methods
+//    that read X twice (CholQR2, SVQB2) and for explicit plans whose blocks exceed a slab.
+//  * stream_slabs: single-pass methods see X as a sequence of row slabs moving through a ring of
+//    ctx->kRing device buffers: slab i+1 .. i+2 are in flight over PCIe while slab i is factored, and
+//    device memory stays O(slab) - the reference's streaming state is O((b+n)*n), tsqr.cpp:143-147.
+long long even_up(long long v) { return (v + 1) & ~1ll; }
 
-int upload_slabs(sqb_context* ctx, const double* x, long long m, int n, long long ld,
-                 long long row_align, const std::function<int(long long, long long)>& on_slab) {
-  SQB_TRY(grow(&ctx->xbuf, &ctx->xbuf_doubles, static_cast<size_t>(m) * n + 2));
-  long long slab_rows = static_cast<long long>(kSlabBytes / (sizeof(double) * n));
-  slab_rows = std::max(row_align, slab_rows / row_align * row_align);
+int upload_resident(sqb_context* ctx, const double* x, long long m, int n, long long ld, int extra_cols,
+                    long long* ldx) {
+  *ldx = even_up(std::max<long long>(m, 1));
+  SQB_TRY(grow(&ctx->xbuf, &ctx->xbuf_doubles, static_cast<size_t>(*ldx) * (n + extra_cols)));
+  const long long slab_rows = std::max<long long>(2, ctx->host_slab_bytes / (sizeof(double) * n) / 2 * 2);
   for (long long r0 = 0; r0 < m; r0 += slab_rows) {
     const long long rows = std::min(slab_rows, m - r0);
-    SQB_CUDA(cudaMemcpy2DAsync(ctx->xbuf + r0, sizeof(double) * m, x + r0, sizeof(double) * ld,
+    SQB_CUDA(cudaMemcpy2DAsync(ctx->xbuf + r0, sizeof(double) * *ldx, x + r0, sizeof(double) * ld,
                                sizeof(double) * rows, n, cudaMemcpyHostToDevice, ctx->copy_stream));
+  }
+  SQB_CUDA(cudaEventRecord(ctx->slab_ready, ctx->copy_stream));
+  SQB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->slab_ready, 0));
+  return SQB_OK;
+}
+
+using SlabFn = std::function<int(long long slab, long long r0, long long rows, const double* d_slab, long long ld_slab)>;
+
+// rows per slab: a multiple of `row_align` (>= 2, even) that fits host_slab_bytes for n_tot columns
+long long slab_rows_for(const sqb_context* ctx, int n_tot, long long row_align) {
+  const long long want = ctx->host_slab_bytes / (static_cast<long long>(sizeof(double)) * n_tot);
+  return std::max(row_align, want / row_align * row_align);
+}
+
+// `extra` (optional) is one more host column of m entries that travels as column n of every slab
+// (least squares: the [A rhs] pencil, lstsq.cpp:24-26).
+int stream_slabs(sqb_context* ctx, const double* x, const double* extra, long long m, int n, long long ld,
+                 long long slab_rows, const SlabFn& on_slab) {
+  const int n_tot = n + (extra ? 1 : 0);
+  const long long lds = even_up(slab_rows);
+  const size_t slab_doubles = static_cast<size_t>(lds) * n_tot;
+  SQB_TRY(grow(&ctx->ring, &ctx->ring_doubles, slab_doubles * sqb_context::kRing));
+  // the ring may still be read by kernels of an earlier call on this stream
+  SQB_CUDA(cudaEventRecord(ctx->slab_ready, ctx->stream));
+  SQB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->slab_ready, 0));
+  long long slab = 0;
+  for (long long r0 = 0; r0 < m; r0 += slab_rows, ++slab) {
+    const long long rows = std::min(slab_rows, m - r0);
+    const int slot = static_cast<int>(slab % sqb_context::kRing);
+    double* dst = ctx->ring + slab_doubles * slot;
+    if (slab >= sqb_context::kRing) SQB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->ring_free[slot], 0));
+    SQB_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * lds, x + r0, sizeof(double) * ld, sizeof(double) * rows, n,
+                               cudaMemcpyHostToDevice, ctx->copy_stream));
+    if (extra)
+      SQB_CUDA(cudaMemcpyAsync(dst + static_cast<size_t>(lds) * n, extra + r0, sizeof(double) * rows,
+                               cudaMemcpyHostToDevice, ctx->copy_stream));
     SQB_CUDA(cudaEventRecord(ctx->slab_ready, ctx->copy_stream));
     SQB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->slab_ready, 0));
-    if (on_slab) SQB_TRY(on_slab(r0, rows));
+    SQB_TRY(on_slab(slab, r0, rows, dst, lds));
+    SQB_CUDA(cudaEventRecord(ctx->ring_free[slot], ctx->stream));
   }
+  return SQB_OK;
+}
+
+// Every *_host call starts from a clean status word: an error left behind by an un-synchronised
+// *_dev call must not be attributed to this call.
+int enter_host(sqb_context* ctx) {
+  SQB_TRY(enter(ctx));
+  SQB_CUDA(cudaMemsetAsync(ctx->d_status, 0, sizeof(StatusWord), ctx->stream));
   return SQB_OK;
 }
 
@@ -351,13 +402,17 @@ NcclApi& nccl() {
   return api;
 }
 
-int allreduce_square(sqb_context* ctx, double* d, int n) {
-  if (ctx->world <= 1 && !ctx->nccl_comm) return SQB_OK;  // an attached 1-rank communicator is used
+// ---- the n x n exchange of the row-sharded drivers ---------------------------------------------------
+bool is_sharded(const sqb_context* ctx) { return ctx->world > 1 || ctx->nccl_comm || ctx->gather_fn; }
+
+// `count` doubles per rank: send -> recv (world blocks in rank order).  One implementation of the
+// protocol, two transports: a caller-supplied all-gather or NCCL.
+int allgather_blocks(sqb_context* ctx, const double* send, double* recv, size_t count) {
+  if (ctx->gather_fn)
+    return ctx->gather_fn(ctx->gather_user, send, recv, static_cast<int64_t>(count)) == 0 ? SQB_OK : SQB_E_NCCL;
   NcclApi& api = nccl();
   if (!api.ok || !ctx->nccl_comm) return SQB_E_NCCL;
-  const int rc = api.AllReduce(d, d, static_cast<size_t>(n) * n, kNcclFloat64, kNcclSum,
-                               ctx->nccl_comm, ctx->stream);
-  return rc == 0 ? SQB_OK : SQB_E_NCCL;
+  return api.AllGather(send, recv, count, kNcclFloat64, ctx->nccl_comm, ctx->stream) == 0 ? SQB_OK : SQB_E_NCCL;
 }
 
 // gathered: world blocks of n x n (column-major, leading dimension n) -> (world*n) x n stack
@@ -373,31 +428,72 @@ __global__ void pack_stack_kernel(const double* __restrict__ gathered, int world
   }
 }
 
+// out = sum over ranks, ascending rank order (the reference's ascending block order, gram.cpp:81-92):
+// every rank computes the same sum bit for bit, whatever the transport's internal order is
+__global__ void sum_ranks_kernel(const double* __restrict__ gathered, int world, long long count,
+                                 double* __restrict__ out) {
+  for (long long t = threadIdx.x + static_cast<long long>(blockIdx.x) * blockDim.x; t < count;
+       t += static_cast<long long>(blockDim.x) * gridDim.x) {
+    double acc = gathered[t];
+    for (int g = 1; g < world; ++g) acc += gathered[t + g * count];
+    out[t] = acc;
+  }
+}
+
+// Stage 2 with k = world (tsqr.cpp:193-195): stack the gathered triangles, fold, sign-normalise.
+int tsqr_combine(sqb_context* ctx, const double* gathered, int world, int n, double* stack, double* d_r) {
+  pack_stack_kernel<<<8, 256, 0, ctx->stream>>>(gathered, world, n, stack);
+  SQB_CUDA(cudaGetLastError());
+  ctx->launches++;
+  const long long rows = static_cast<long long>(world) * n;
+  return launch_tsqr(ctx, plain_view(stack, rows, n), rows, n, make_plan(rows, 1, rows), d_r, n, true, false);
+}
+
+int gram_combine(sqb_context* ctx, const double* gathered, int world, int n, double* d_c) {
+  const long long count = static_cast<long long>(n) * n;
+  sum_ranks_kernel<<<static_cast<unsigned>(std::min<long long>((count + 255) / 256, 64)), 256, 0, ctx->stream>>>(
+      gathered, world, count, d_c);
+  SQB_CUDA(cudaGetLastError());
+  ctx->launches++;
+  return SQB_OK;
+}
+
+// scratch of the exchange: [gathered: world*n*n][stack: world*n*n]
+int exchange_scratch(sqb_context* ctx, int n, double** gathered, double** stack) {
+  const size_t nn = static_cast<size_t>(n) * n;
+  SQB_TRY(grow(&ctx->gen, &ctx->gen_doubles, 2 * nn * ctx->world));
+  *gathered = ctx->gen;
+  *stack = ctx->gen + nn * ctx->world;
+  return SQB_OK;
+}
+
+// Partial Gram of this rank's slab (in place in d) -> the sum over all ranks, identical everywhere.
+int allreduce_square(sqb_context* ctx, double* d, int n) {
+  if (!is_sharded(ctx)) return SQB_OK;
+  double *gathered, *stack;
+  SQB_TRY(exchange_scratch(ctx, n, &gathered, &stack));
+  SQB_TRY(allgather_blocks(ctx, d, gathered, static_cast<size_t>(n) * n));
+  return gram_combine(ctx, gathered, ctx->world, n, d);
+}
+
+// This rank's un-normalised triangle; a rank may own fewer than n rows (or none): its triangle is
+// then that of a zero-padded slab.
+int tsqr_local_view(sqb_context* ctx, const MatView& v, long long m_local, int n, double* d_r_local) {
+  if (m_local > 0) return tsqr_view(ctx, v, m_local, n, 0, 0, d_r_local, false);
+  SQB_CUDA(cudaMemsetAsync(d_r_local, 0, sizeof(double) * n * n, ctx->stream));
+  return SQB_OK;
+}
+
 // Local triangle -> all-gather -> redundant final combine on every rank (stage 2 with k = world).
 int tsqr_sharded_view(sqb_context* ctx, const MatView& v, long long m_local, int n, double* d_r) {
-  if (ctx->world <= 1 && !ctx->nccl_comm) return tsqr_view(ctx, v, m_local, n, 0, 0, d_r, true);
-  NcclApi& api = nccl();
-  if (!api.ok || !ctx->nccl_comm) return SQB_E_NCCL;
+  if (!is_sharded(ctx)) return tsqr_view(ctx, v, m_local, n, 0, 0, d_r, true);
   Small s;
   SQB_TRY(small_slots(ctx, n, &s));
-  const size_t nn = static_cast<size_t>(n) * n;
-  // a rank may own fewer than n rows (or none): its triangle is then that of a zero-padded slab
-  if (m_local > 0) {
-    SQB_TRY(tsqr_view(ctx, v, m_local, n, 0, 0, s.c1, false));
-  } else {
-    SQB_CUDA(cudaMemsetAsync(s.c1, 0, nn * sizeof(double), ctx->stream));
-  }
-  const size_t need = 2 * nn * ctx->world;
-  SQB_TRY(grow(&ctx->gen, &ctx->gen_doubles, need));
-  double* gathered = ctx->gen;
-  double* stack = ctx->gen + nn * ctx->world;
-  if (api.AllGather(s.c1, gathered, nn, kNcclFloat64, ctx->nccl_comm, ctx->stream) != 0)
-    return SQB_E_NCCL;
-  pack_stack_kernel<<<8, 256, 0, ctx->stream>>>(gathered, ctx->world, n, stack);
-  ctx->launches++;
-  const long long rows = static_cast<long long>(ctx->world) * n;
-  return launch_tsqr(ctx, plain_view(stack, rows, n), rows, n, make_plan(rows, 1, rows), d_r, n, true,
-                     false);
+  SQB_TRY(tsqr_local_view(ctx, v, m_local, n, s.c1));
+  double *gathered, *stack;
+  SQB_TRY(exchange_scratch(ctx, n, &gathered, &stack));
+  SQB_TRY(allgather_blocks(ctx, s.c1, gathered, static_cast<size_t>(n) * n));
+  return tsqr_combine(ctx, gathered, ctx->world, n, stack, d_r);
 }
 
 }  // namespace
@@ -423,6 +519,9 @@ int sqb_create(sqb_context** out, int device) {
   bool ok = cudaStreamCreateWithFlags(&ctx->own_stream_handle, cudaStreamNonBlocking) == cudaSuccess &&
             cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) == cudaSuccess &&
             cudaEventCreateWithFlags(&ctx->slab_ready, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ctx->ring_free[0], cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ctx->ring_free[1], cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ctx->ring_free[2], cudaEventDisableTiming) == cudaSuccess &&
             cudaMalloc(reinterpret_cast<void**>(&ctx->d_status), sizeof(StatusWord)) == cudaSuccess &&
             cudaMallocHost(reinterpret_cast<void**>(&ctx->h_status), sizeof(StatusWord)) == cudaSuccess;
   if (ok) ok = cudaMemset(ctx->d_status, 0, sizeof(StatusWord)) == cudaSuccess;
@@ -444,6 +543,9 @@ int sqb_destroy(sqb_context* ctx) {
   cudaFree(ctx->work);
   cudaFree(ctx->small);
   cudaFree(ctx->xbuf);
+  cudaFree(ctx->ring);
+  for (cudaEvent_t e : ctx->ring_free)
+    if (e) cudaEventDestroy(e);
   cudaFree(ctx->gen);
   cudaFree(ctx->d_status);
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
@@ -469,6 +571,34 @@ int sqb_use_own_stream(sqb_context* ctx) {
 }
 
 void* sqb_get_stream(sqb_context* ctx) { return ctx ? ctx->stream : nullptr; }
+
+int sqb_set_tsqr_kernel(sqb_context* ctx, int kind) {
+  if (!ctx || kind < kTsqrAuto || kind > kTsqrMma) return SQB_E_ARGUMENT;
+  ctx->tsqr_kind = kind;
+  return SQB_OK;
+}
+
+int sqb_set_host_slab_bytes(sqb_context* ctx, int64_t bytes) {
+  if (!ctx || bytes < (1ll << 20)) return SQB_E_ARGUMENT;
+  ctx->host_slab_bytes = bytes;
+  return SQB_OK;
+}
+
+int sqb_copy_h2d(sqb_context* ctx, void* d_dst, const void* h_src, int64_t bytes) {
+  SQB_TRY(enter(ctx));
+  if (bytes < 0 || (bytes > 0 && (!d_dst || !h_src))) return SQB_E_ARGUMENT;
+  SQB_CUDA(cudaMemcpyAsync(d_dst, h_src, static_cast<size_t>(bytes), cudaMemcpyHostToDevice, ctx->stream));
+  SQB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return SQB_OK;
+}
+
+int sqb_copy_d2h(sqb_context* ctx, void* h_dst, const void* d_src, int64_t bytes) {
+  SQB_TRY(enter(ctx));
+  if (bytes < 0 || (bytes > 0 && (!h_dst || !d_src))) return SQB_E_ARGUMENT;
+  SQB_CUDA(cudaMemcpyAsync(h_dst, d_src, static_cast<size_t>(bytes), cudaMemcpyDeviceToHost, ctx->stream));
+  SQB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return SQB_OK;
+}
 
 int sqb_sync(sqb_context* ctx) {
   SQB_TRY(enter(ctx));
@@ -545,7 +675,7 @@ int sqb_block_qless_qr_dev(sqb_context* ctx, const double* d_x, int64_t m, int64
                            int64_t panel_rows, double* d_r) {
   SQB_TRY(enter(ctx));
   if (n < 1 || n > 64 || ld < m || m < 0) return SQB_E_ARGUMENT;
-  const int64_t b = panel_rows > 0 ? panel_rows : tsqr_panel_rows(static_cast<int>(n));
+  const int64_t b = panel_rows > 0 ? panel_rows : tsqr_panel_rows(static_cast<int>(n), ctx->tsqr_kind);
   Plan p{1, b, ceil_div(std::max<int64_t>(m, 1), b) * b};
   return launch_tsqr(ctx, plain_view(d_x, ld, static_cast<int>(n)), m, static_cast<int>(n), p, d_r, n,
                      false, true);
@@ -556,15 +686,16 @@ static int gram_entry(sqb_context* ctx, const double* d_x, int64_t m, int64_t n,
   SQB_TRY(enter(ctx));
   if (n < 1 || m < 0) return SQB_E_DIMENSION;
   if (ld < m) return SQB_E_ARGUMENT;
-  if (n > 64) {
-    // the reference's Gram kernels have no column limit (gram.cpp:113-151); here the plain Gram goes
-    // up to 256 columns and the fused solve + Gram up to 128; the fused multiply stays at n <= 64
-    return gram_wide_view(ctx, plain_view(d_x, ld, static_cast<int>(n)), m, static_cast<int>(n), op, factor, d_c,
-                          op == OP_PLAIN);
-  }
-  if (op == OP_MULTIPLY) {  // tsmmttsmm checks B for finiteness (gram.cpp:143-145)
+  if (op == OP_MULTIPLY) {  // tsmmttsmm checks B for finiteness at any n (gram.cpp:143-145)
+    if (n > kWideFusedMaxN) return SQB_E_ARGUMENT;
     SQB_CUDA(launch_check_finite(factor, n * n, ctx->d_status, ctx->stream));
     ctx->launches++;
+  }
+  if (n > 64) {
+    // the reference's Gram kernels have no column limit (gram.cpp:113-151); here the plain Gram goes
+    // up to 256 columns, the fused solve / multiply + Gram up to 128
+    return gram_wide_view(ctx, plain_view(d_x, ld, static_cast<int>(n)), m, static_cast<int>(n), op, factor, d_c,
+                          op == OP_PLAIN);
   }
   return gram_view(ctx, plain_view(d_x, ld, static_cast<int>(n)), m, static_cast<int>(n), op, factor, k,
                    b, d_c, op == OP_PLAIN);
@@ -711,81 +842,161 @@ int sqb_solve_lstsq_dev(sqb_context* ctx, const double* d_a, int64_t m, int64_t 
 }
 
 // ---- host-pointer entry points -------------------------------------------------------------------
+// Slab layout for a single-pass call under a plan.  Default plan (k = b = 0): every slab is cut into
+// its own blocks.  Explicit plan: the reference partition (plan.hpp:24-37) is reproduced exactly by
+// making every slab a whole number of plan blocks; *resident is set when one block alone exceeds the
+// slab budget (then X is uploaded whole).
+struct SlabPlan {
+  long long slab_rows;   // rows per slab
+  long long blocks;      // kernel blocks (CTAs) per full slab
+  long long rpb;         // rows per block inside a slab
+  bool resident;
+};
+
+SlabPlan slab_plan(const sqb_context* ctx, long long m, int n_tot, long long k, long long b, long long P,
+                   long long NW, int ctas_per_sm) {
+  SlabPlan sp{0, 0, 0, false};
+  if (k > 0 || b > 0) {
+    if (k <= 0) k = 1;
+    if (b <= 0) b = P;
+    sp.rpb = make_plan(m, k, b).rpb;
+    const long long budget = ctx->host_slab_bytes / (static_cast<long long>(sizeof(double)) * n_tot);
+    sp.blocks = std::min(k, budget / std::max<long long>(sp.rpb, 1));
+    if (sp.blocks < 1 || (sp.rpb & 1)) {  // odd block heights would leave later blocks unaligned inside a slab
+      sp.resident = true;
+      return sp;
+    }
+    sp.slab_rows = sp.blocks * sp.rpb;
+    return sp;
+  }
+  sp.slab_rows = slab_rows_for(ctx, n_tot, even_up(P));
+  sp.blocks = std::max<long long>(1, std::min<long long>(ctx->sm_count * ctas_per_sm, sp.slab_rows / (P * NW)));
+  sp.rpb = make_plan(sp.slab_rows, sp.blocks, P).rpb;
+  return sp;
+}
+
+// Q-less TSQR of a host matrix (optionally with one extra host column): slabs are factored as they
+// land, all block triangles are stacked in ctx->work and reduced by the stage-2 tree.
+int tsqr_host_stream(sqb_context* ctx, const double* x, const double* extra, long long m, int n, long long ld,
+                     long long k, long long b, double* d_r, bool finalize) {
+  const int nt = n + (extra ? 1 : 0);
+  const long long P = tsqr_panel_rows(nt, ctx->tsqr_kind), NW = tsqr_warps(nt, ctx->tsqr_kind);
+  const SlabPlan sp = slab_plan(ctx, m, nt, k, b, P, NW, 1);
+  if (sp.resident) {
+    long long ldx = 0;
+    SQB_TRY(upload_resident(ctx, x, m, n, ld, extra ? 1 : 0, &ldx));
+    MatView v = plain_view(ctx->xbuf, ldx, nt);
+    if (extra) {
+      SQB_CUDA(cudaMemcpyAsync(ctx->xbuf + static_cast<size_t>(ldx) * n, extra, sizeof(double) * m,
+                               cudaMemcpyHostToDevice, ctx->stream));
+    }
+    return tsqr_view(ctx, v, m, nt, k, b, d_r, finalize);
+  }
+  const long long nslabs = std::max<long long>(1, ceil_div(m, sp.slab_rows));
+  const long long ldy = nslabs * sp.blocks * nt;
+  const size_t ymax = static_cast<size_t>(ldy) * nt;
+  SQB_TRY(grow(&ctx->work, &ctx->work_doubles, 2 * ymax));
+  SQB_CUDA(cudaMemsetAsync(ctx->work, 0, ymax * sizeof(double), ctx->stream));
+  SQB_TRY(stream_slabs(ctx, x, extra, m, n, ld, sp.slab_rows,
+                       [&](long long slab, long long, long long rows, const double* d_slab, long long lds) {
+                         Plan p{std::min(sp.blocks, std::max<long long>(1, ceil_div(rows, sp.rpb))), 0, sp.rpb};
+                         return launch_tsqr(ctx, plain_view(d_slab, lds, nt), rows, nt, p,
+                                            ctx->work + slab * sp.blocks * nt, ldy, false, true);
+                       }));
+  return reduce_stack(ctx, ctx->work, ldy, ldy, nt, ctx->work + ymax, d_r, finalize);
+}
+
 int sqb_tsqr_qless_host(sqb_context* ctx, const double* x, int64_t m, int64_t n, int64_t ld,
                         int64_t num_blocks, int64_t panel_rows, double* r) {
-  SQB_TRY(enter(ctx));
+  SQB_TRY(enter_host(ctx));
   SQB_TRY(check_shape(m, n, ld, 64));
   const int nn = static_cast<int>(n);
   Small s;
   SQB_TRY(small_slots(ctx, nn, &s));
-  if (num_blocks > 0 || panel_rows > 0) {
-    // explicit plan: reproduce the reference partition exactly on the resident copy
-    SQB_TRY(upload_slabs(ctx, x, m, nn, ld, 2, nullptr));
-    SQB_TRY(tsqr_view(ctx, plain_view(ctx->xbuf, m, nn), m, nn, num_blocks, panel_rows, s.rr, true));
-  } else {
-    // default plan: every slab is factored as soon as it lands; all slab triangles are stacked
-    const long long P = tsqr_panel_rows(nn), NW = tsqr_warps(nn);
-    long long slab_rows = static_cast<long long>(kSlabBytes / (sizeof(double) * n));
-    slab_rows = std::max(P, slab_rows / P * P);
-    const long long nslabs = ceil_div(m, slab_rows);
-    const long long kmax = std::max<long long>(1, std::min<long long>(ctx->sm_count, slab_rows / (P * NW)));
-    const size_t ymax = static_cast<size_t>(nslabs) * kmax * nn * nn;
-    SQB_TRY(grow(&ctx->work, &ctx->work_doubles, 2 * ymax));
-    const long long ldy = nslabs * kmax * nn;
-    SQB_CUDA(cudaMemsetAsync(ctx->work, 0, ymax * sizeof(double), ctx->stream));
-    long long slab = 0;
-    SQB_TRY(upload_slabs(ctx, x, m, nn, ld, P, [&](long long r0, long long rows) {
-      const long long k = std::max<long long>(1, std::min<long long>(kmax, rows / (P * NW)));
-      const Plan p = make_plan(rows, k, P);
-      const int st = launch_tsqr(ctx, plain_view(ctx->xbuf + r0, m, nn), rows, nn, p,
-                                 ctx->work + slab * kmax * nn, ldy, false, true);
-      ++slab;
-      return st;
-    }));
-    SQB_TRY(reduce_stack(ctx, ctx->work, ldy, ldy, nn, ctx->work + ymax, s.rr, true));
-  }
+  SQB_TRY(tsqr_host_stream(ctx, x, nullptr, m, nn, ld, num_blocks, panel_rows, s.rr, true));
   SQB_TRY(download(ctx, r, s.rr, sizeof(double) * nn * nn));
   return sqb_sync(ctx);
 }
 
 int sqb_tsqr_stage1_host(sqb_context* ctx, const double* x, int64_t m, int64_t n, int64_t ld,
                          int64_t num_blocks, int64_t panel_rows, double* y) {
-  SQB_TRY(enter(ctx));
+  SQB_TRY(enter_host(ctx));
   if (n < 1 || n > 64 || ld < m || m < 0) return SQB_E_ARGUMENT;
   const int nn = static_cast<int>(n);
   const Plan p = tsqr_plan(ctx, m, nn, num_blocks, panel_rows);
-  SQB_TRY(upload_slabs(ctx, x, m, nn, ld, 2, nullptr));
   const size_t yd = static_cast<size_t>(p.k) * nn * nn;
   SQB_TRY(grow(&ctx->work, &ctx->work_doubles, yd));
-  SQB_TRY(launch_tsqr(ctx, plain_view(ctx->xbuf, m, nn), m, nn, p, ctx->work, p.k * nn, false, true));
+  const long long budget = ctx->host_slab_bytes / (static_cast<long long>(sizeof(double)) * nn);
+  const long long per_slab = std::min(p.k, budget / std::max<long long>(p.rpb, 1));
+  if (per_slab < 1 || (p.rpb & 1)) {
+    long long ldx = 0;
+    SQB_TRY(upload_resident(ctx, x, m, nn, ld, 0, &ldx));
+    SQB_TRY(launch_tsqr(ctx, plain_view(ctx->xbuf, ldx, nn), m, nn, p, ctx->work, p.k * nn, false, true));
+  } else {
+    // block i of the plan is block (i mod per_slab) of slab i / per_slab; blocks past the end of X are empty
+    SQB_CUDA(cudaMemsetAsync(ctx->work, 0, yd * sizeof(double), ctx->stream));
+    SQB_TRY(stream_slabs(ctx, x, nullptr, m, nn, ld, per_slab * p.rpb,
+                         [&](long long slab, long long, long long rows, const double* d_slab, long long lds) {
+                           Plan ps{std::min(per_slab, p.k - slab * per_slab), 0, p.rpb};
+                           return launch_tsqr(ctx, plain_view(d_slab, lds, nn), rows, nn, ps,
+                                              ctx->work + slab * per_slab * nn, p.k * nn, false, true);
+                         }));
+  }
   SQB_TRY(download(ctx, y, ctx->work, yd * sizeof(double)));
   return sqb_sync(ctx);
 }
 
 int sqb_block_qless_qr_host(sqb_context* ctx, const double* x, int64_t m, int64_t n, int64_t ld,
                             int64_t panel_rows, double* r) {
-  SQB_TRY(enter(ctx));
+  SQB_TRY(enter_host(ctx));
   if (n < 1 || n > 64 || ld < m || m < 0) return SQB_E_ARGUMENT;
   const int nn = static_cast<int>(n);
   Small s;
   SQB_TRY(small_slots(ctx, nn, &s));
-  SQB_TRY(upload_slabs(ctx, x, m, nn, ld, 2, nullptr));
-  SQB_TRY(sqb_block_qless_qr_dev(ctx, ctx->xbuf, m, n, m, panel_rows, s.rr));
+  long long ldx = 0;  // one block = one CTA walking all of X: resident copy
+  SQB_TRY(upload_resident(ctx, x, m, nn, ld, 0, &ldx));
+  SQB_TRY(sqb_block_qless_qr_dev(ctx, ctx->xbuf, m, n, ldx, panel_rows, s.rr));
   SQB_TRY(download(ctx, r, s.rr, sizeof(double) * nn * nn));
   return sqb_sync(ctx);
 }
 
 static int gram_host(sqb_context* ctx, const double* x, int64_t m, int64_t n, int64_t ld, int op,
                      const double* factor, int64_t k, int64_t b, double* c) {
-  SQB_TRY(enter(ctx));
+  SQB_TRY(enter_host(ctx));
   if (n < 1 || m < 0) return SQB_E_DIMENSION;
   if (n > (op == OP_PLAIN ? kWideGramMaxN : kWideFusedMaxN) || ld < m) return SQB_E_ARGUMENT;
   const int nn = static_cast<int>(n);
   Small s;
   SQB_TRY(small_slots(ctx, nn, &s));
   if (factor) SQB_TRY(upload_small(ctx, factor, static_cast<size_t>(nn) * nn, s.r1));
-  SQB_TRY(upload_slabs(ctx, x, m, nn, ld, 2, nullptr));
-  SQB_TRY(gram_entry(ctx, ctx->xbuf, m, n, m, op, factor ? s.r1 : nullptr, k, b, s.rr));
+  const double* d_factor = factor ? s.r1 : nullptr;
+  SlabPlan sp{0, 0, 0, true};
+  if (nn <= 64) sp = slab_plan(ctx, m, nn, k, b, gram_panel_rows(nn, op), gram_warps(nn), gram_ctas_per_sm(nn, op));
+  if (sp.resident) {  // wide kernels (own row partition) and oversized explicit blocks
+    long long ldx = 0;
+    SQB_TRY(upload_resident(ctx, x, m, nn, ld, 0, &ldx));
+    SQB_TRY(gram_entry(ctx, ctx->xbuf, m, n, ldx, op, d_factor, k, b, s.rr));
+  } else {
+    if (op == OP_MULTIPLY) {  // tsmmttsmm checks B for finiteness (gram.cpp:143-145)
+      SQB_CUDA(launch_check_finite(d_factor, n * n, ctx->d_status, ctx->stream));
+      ctx->launches++;
+    }
+    // per-block partial Grams of all slabs, summed in ascending block order by one reduce launch
+    const long long nslabs = std::max<long long>(1, ceil_div(m, sp.slab_rows));
+    const size_t pd = static_cast<size_t>(nslabs) * sp.blocks * nn * nn;
+    SQB_TRY(grow(&ctx->work, &ctx->work_doubles, pd));
+    SQB_CUDA(cudaMemsetAsync(ctx->work, 0, pd * sizeof(double), ctx->stream));
+    SQB_TRY(stream_slabs(ctx, x, nullptr, m, nn, ld, sp.slab_rows,
+                         [&](long long slab, long long, long long rows, const double* d_slab, long long lds) {
+                           Plan p{std::min(sp.blocks, std::max<long long>(1, ceil_div(rows, sp.rpb))), 0, sp.rpb};
+                           return launch_gram_blocks(ctx, plain_view(d_slab, lds, nn), rows, nn, op, d_factor, p,
+                                                     ctx->work + static_cast<size_t>(slab) * sp.blocks * nn * nn,
+                                                     op == OP_PLAIN);
+                         }));
+    SQB_CUDA(launch_gram_reduce(ctx->work, nslabs * sp.blocks, nn, s.rr, op == OP_PLAIN ? 1 : 0, ctx->d_status,
+                                ctx->stream));
+    ctx->launches++;
+  }
   SQB_TRY(download(ctx, c, s.rr, sizeof(double) * nn * nn));
   return sqb_sync(ctx);
 }
@@ -804,7 +1015,7 @@ int sqb_tsmmttsmm_host(sqb_context* ctx, const double* x, int64_t m, int64_t n, 
 }
 
 int sqb_cholesky_host(sqb_context* ctx, const double* c, int64_t n, double* r) {
-  SQB_TRY(enter(ctx));
+  SQB_TRY(enter_host(ctx));
   if (n < 1) return SQB_E_DIMENSION;
   if (n > kSmallMaxN) return SQB_E_ARGUMENT;
   Small s;
@@ -817,7 +1028,7 @@ int sqb_cholesky_host(sqb_context* ctx, const double* c, int64_t n, double* r) {
 
 int sqb_eigh_small_host(sqb_context* ctx, const double* c, int64_t n, double* values,
                         double* vectors) {
-  SQB_TRY(enter(ctx));
+  SQB_TRY(enter_host(ctx));
   if (n < 1) return SQB_E_DIMENSION;
   if (n > kSmallMaxN) return SQB_E_ARGUMENT;
   Small s;
@@ -831,21 +1042,22 @@ int sqb_eigh_small_host(sqb_context* ctx, const double* c, int64_t n, double* va
 
 int sqb_cholqr2_host(sqb_context* ctx, const double* x, int64_t m, int64_t n, int64_t ld,
                      int64_t num_blocks, int64_t panel_rows, double* r) {
-  SQB_TRY(enter(ctx));
+  SQB_TRY(enter_host(ctx));
   SQB_TRY(check_shape(m, n, ld, kWideFusedMaxN));
   const int nn = static_cast<int>(n);
   Small s;
   SQB_TRY(small_slots(ctx, nn, &s));
-  SQB_TRY(upload_slabs(ctx, x, m, nn, ld, 2, nullptr));
-  if (nn > 64) SQB_TRY(cholqr2_wide(ctx, plain_view(ctx->xbuf, m, nn), m, nn, s.rr, nullptr));
-  else SQB_TRY(cholqr2_view(ctx, plain_view(ctx->xbuf, m, nn), m, nn, num_blocks, panel_rows, s.rr, nullptr));
+  long long ldx = 0;  // X is read twice: resident copy
+  SQB_TRY(upload_resident(ctx, x, m, nn, ld, 0, &ldx));
+  if (nn > 64) SQB_TRY(cholqr2_wide(ctx, plain_view(ctx->xbuf, ldx, nn), m, nn, s.rr, nullptr));
+  else SQB_TRY(cholqr2_view(ctx, plain_view(ctx->xbuf, ldx, nn), m, nn, num_blocks, panel_rows, s.rr, nullptr));
   SQB_TRY(download(ctx, r, s.rr, sizeof(double) * nn * nn));
   return sqb_sync(ctx);
 }
 
 int sqb_svqb_pass_host(sqb_context* ctx, const double* c, int64_t n, double* b, double* z,
                        double* sigma, int64_t* rank) {
-  SQB_TRY(enter(ctx));
+  SQB_TRY(enter_host(ctx));
   if (n < 1) return SQB_E_DIMENSION;
   if (n > kSmallMaxN) return SQB_E_ARGUMENT;
   Small s;
@@ -862,17 +1074,18 @@ int sqb_svqb_pass_host(sqb_context* ctx, const double* c, int64_t n, double* b, 
 int sqb_svqb2_host(sqb_context* ctx, const double* x, int64_t m, int64_t n, int64_t ld,
                    int64_t num_blocks, int64_t panel_rows, double* transform, double* z,
                    double* sigma, int64_t* rank) {
-  SQB_TRY(enter(ctx));
+  SQB_TRY(enter_host(ctx));
   SQB_TRY(check_shape(m, n, ld, kWideFusedMaxN));
   const int nn = static_cast<int>(n);
   const size_t sq = static_cast<size_t>(nn) * nn;
   Small s;
   SQB_TRY(small_slots(ctx, nn, &s));
-  SQB_TRY(upload_slabs(ctx, x, m, nn, ld, 2, nullptr));
+  long long ldx = 0;
+  SQB_TRY(upload_resident(ctx, x, m, nn, ld, 0, &ldx));
   if (nn > 64)
-    SQB_TRY(svqb2_wide(ctx, plain_view(ctx->xbuf, m, nn), m, nn, s.rr, s.rr + sq, s.s2 + nn, s.rank1 + 1, nullptr));
+    SQB_TRY(svqb2_wide(ctx, plain_view(ctx->xbuf, ldx, nn), m, nn, s.rr, s.rr + sq, s.s2 + nn, s.rank1 + 1, nullptr));
   else
-    SQB_TRY(svqb2_view(ctx, plain_view(ctx->xbuf, m, nn), m, nn, num_blocks, panel_rows, s.rr, s.rr + sq,
+    SQB_TRY(svqb2_view(ctx, plain_view(ctx->xbuf, ldx, nn), m, nn, num_blocks, panel_rows, s.rr, s.rr + sq,
                        s.s2 + nn, s.rank1 + 1, nullptr));
   SQB_TRY(download(ctx, transform, s.rr, sizeof(double) * sq));
   SQB_TRY(download(ctx, z, s.rr + sq, sizeof(double) * sq));
@@ -883,37 +1096,46 @@ int sqb_svqb2_host(sqb_context* ctx, const double* x, int64_t m, int64_t n, int6
 
 int sqb_reconstruct_q_host(sqb_context* ctx, const double* x, int64_t m, int64_t n, int64_t ld,
                            const double* r, double* q, int64_t ldq) {
-  SQB_TRY(enter(ctx));
+  SQB_TRY(enter_host(ctx));
   if (n < 1 || m < 0) return SQB_E_DIMENSION;
   if (n > kWideFusedMaxN || ld < m || ldq < m) return SQB_E_ARGUMENT;
   const int nn = static_cast<int>(n);
   Small s;
   SQB_TRY(small_slots(ctx, nn, &s));
   SQB_TRY(upload_small(ctx, r, static_cast<size_t>(nn) * nn, s.r1));
-  SQB_TRY(upload_slabs(ctx, x, m, nn, ld, 2, nullptr));
-  SQB_TRY(grow(&ctx->gen, &ctx->gen_doubles, static_cast<size_t>(m) * nn));
-  SQB_TRY(sqb_reconstruct_q_dev(ctx, ctx->xbuf, m, n, m, s.r1, ctx->gen, m));
-  SQB_CUDA(cudaMemcpy2DAsync(q, sizeof(double) * ldq, ctx->gen, sizeof(double) * m, sizeof(double) * m,
+  long long ldx = 0;
+  SQB_TRY(upload_resident(ctx, x, m, nn, ld, 0, &ldx));
+  SQB_TRY(grow(&ctx->gen, &ctx->gen_doubles, static_cast<size_t>(ldx) * nn));
+  SQB_TRY(sqb_reconstruct_q_dev(ctx, ctx->xbuf, m, n, ldx, s.r1, ctx->gen, ldx));
+  SQB_CUDA(cudaMemcpy2DAsync(q, sizeof(double) * ldq, ctx->gen, sizeof(double) * ldx, sizeof(double) * m,
                              nn, cudaMemcpyDeviceToHost, ctx->stream));
   return sqb_sync(ctx);
 }
 
 int sqb_solve_lstsq_host(sqb_context* ctx, const double* a, int64_t m, int64_t n, int64_t lda,
                          const double* rhs, int method, double* xsol, double* residual) {
-  SQB_TRY(enter(ctx));
+  SQB_TRY(enter_host(ctx));
   if (n < 1 || m < n + 1) return SQB_E_DIMENSION;
   if (n + 1 > kWideFusedMaxN || lda < m) return SQB_E_ARGUMENT;
   const int nn = static_cast<int>(n);
   Small s;
   SQB_TRY(small_slots(ctx, nn + 1, &s));
-  // [A rhs] lands as one resident (n+1)-column matrix: rhs is simply the last column's slab
-  SQB_TRY(grow(&ctx->xbuf, &ctx->xbuf_doubles, static_cast<size_t>(m) * (nn + 1) + 2));
-  SQB_TRY(upload_slabs(ctx, a, m, nn, lda, 2, nullptr));
-  SQB_CUDA(cudaMemcpyAsync(ctx->xbuf + static_cast<size_t>(m) * nn, rhs, sizeof(double) * m,
-                           cudaMemcpyHostToDevice, ctx->stream));
-  const MatView v{ctx->xbuf, m, ctx->xbuf + static_cast<size_t>(m) * nn, nn};
   double* d_out = s.s2 + 2 * (nn + 1);
-  SQB_TRY(lstsq_view(ctx, v, m, nn + 1, method, d_out, d_out + nn, false));
+  if (method == SQB_METHOD_TSQR) {
+    // single pass: [A rhs] streams through the slab ring, rhs travelling as the last column
+    if (nn + 1 > 64) return SQB_E_ARGUMENT;  // tsqr.cpp:188
+    SQB_TRY(tsqr_host_stream(ctx, a, rhs, m, nn, lda, 0, 0, s.rr, true));
+    SQB_CUDA(launch_backsolve(s.rr, nn + 1, d_out, d_out + nn, ctx->d_status, ctx->stream));
+    ctx->launches++;
+  } else {
+    // two passes: [A rhs] lands as one resident (n+1)-column matrix, rhs in the last column
+    long long ldx = 0;
+    SQB_TRY(upload_resident(ctx, a, m, nn, lda, 1, &ldx));
+    double* d_rhs = ctx->xbuf + static_cast<size_t>(ldx) * nn;
+    SQB_CUDA(cudaMemcpyAsync(d_rhs, rhs, sizeof(double) * m, cudaMemcpyHostToDevice, ctx->stream));
+    const MatView v{ctx->xbuf, ldx, d_rhs, nn};
+    SQB_TRY(lstsq_view(ctx, v, m, nn + 1, method, d_out, d_out + nn, false));
+  }
   SQB_TRY(download(ctx, xsol, d_out, sizeof(double) * nn));
   SQB_TRY(download(ctx, residual, d_out + nn, sizeof(double)));
   return sqb_sync(ctx);
@@ -954,6 +1176,40 @@ int sqb_attach_nccl(sqb_context* ctx, void* nccl_comm, int rank, int world) {
   return SQB_OK;
 }
 
+int sqb_set_allgather(sqb_context* ctx, sqb_allgather_fn fn, void* user, int rank, int world) {
+  SQB_TRY(enter(ctx));
+  if (world < 1 || rank < 0 || rank >= world || (world > 1 && !fn)) return SQB_E_ARGUMENT;
+  ctx->gather_fn = fn;
+  ctx->gather_user = user;
+  ctx->rank = rank;
+  ctx->world = world;
+  return SQB_OK;
+}
+
+int sqb_tsqr_local_dev(sqb_context* ctx, const double* d_x, int64_t m_local, int64_t n, int64_t ld,
+                       double* d_r_local) {
+  SQB_TRY(enter(ctx));
+  if (n < 1 || m_local < 0) return SQB_E_DIMENSION;
+  if (n > 64 || ld < m_local) return SQB_E_ARGUMENT;
+  return tsqr_local_view(ctx, plain_view(d_x, ld, static_cast<int>(n)), m_local, static_cast<int>(n), d_r_local);
+}
+
+int sqb_tsqr_combine_dev(sqb_context* ctx, const double* d_gathered, int64_t world, int64_t n, double* d_r) {
+  SQB_TRY(enter(ctx));
+  if (n < 1 || world < 1) return SQB_E_DIMENSION;
+  if (n > 64 || world > (1 << 20)) return SQB_E_ARGUMENT;
+  const size_t nn = static_cast<size_t>(n) * n;
+  SQB_TRY(grow(&ctx->gen, &ctx->gen_doubles, nn * world));
+  return tsqr_combine(ctx, d_gathered, static_cast<int>(world), static_cast<int>(n), ctx->gen, d_r);
+}
+
+int sqb_gram_combine_dev(sqb_context* ctx, const double* d_gathered, int64_t world, int64_t n, double* d_c) {
+  SQB_TRY(enter(ctx));
+  if (n < 1 || world < 1) return SQB_E_DIMENSION;
+  if (world > (1 << 20)) return SQB_E_ARGUMENT;
+  return gram_combine(ctx, d_gathered, static_cast<int>(world), static_cast<int>(n), d_c);
+}
+
 int sqb_nccl_unique_id(void* out128) {
   if (!out128 || !nccl().ok) return SQB_E_NCCL;
   return nccl().GetUniqueId(static_cast<NcclId*>(out128)) == 0 ? SQB_OK : SQB_E_NCCL;
@@ -981,6 +1237,29 @@ int sqb_tsqr_qless_sharded_dev(sqb_context* ctx, const double* d_x, int64_t m_lo
   if (n > 64 || ld < m_local) return SQB_E_ARGUMENT;
   return tsqr_sharded_view(ctx, plain_view(d_x, ld, static_cast<int>(n)), m_local, static_cast<int>(n),
                            d_r);
+}
+
+// Host slab of this rank -> slab ring -> local triangle -> exchange -> combine -> host R.
+int sqb_tsqr_qless_sharded_host(sqb_context* ctx, const double* x, int64_t m_local, int64_t n, int64_t ld,
+                                double* r) {
+  SQB_TRY(enter_host(ctx));
+  if (n < 1 || m_local < 0) return SQB_E_DIMENSION;
+  if (n > 64 || ld < m_local) return SQB_E_ARGUMENT;
+  const int nn = static_cast<int>(n);
+  Small s;
+  SQB_TRY(small_slots(ctx, nn, &s));
+  if (!is_sharded(ctx)) {
+    SQB_TRY(tsqr_host_stream(ctx, x, nullptr, m_local, nn, ld, 0, 0, s.rr, true));
+  } else {
+    if (m_local > 0) SQB_TRY(tsqr_host_stream(ctx, x, nullptr, m_local, nn, ld, 0, 0, s.c1, false));
+    else SQB_CUDA(cudaMemsetAsync(s.c1, 0, sizeof(double) * nn * nn, ctx->stream));
+    double *gathered, *stack;
+    SQB_TRY(exchange_scratch(ctx, nn, &gathered, &stack));
+    SQB_TRY(allgather_blocks(ctx, s.c1, gathered, static_cast<size_t>(nn) * nn));
+    SQB_TRY(tsqr_combine(ctx, gathered, ctx->world, nn, stack, s.rr));
+  }
+  SQB_TRY(download(ctx, r, s.rr, sizeof(double) * nn * nn));
+  return sqb_sync(ctx);
 }
 
 int sqb_cholqr2_sharded_dev(sqb_context* ctx, const double* d_x, int64_t m_local, int64_t n,

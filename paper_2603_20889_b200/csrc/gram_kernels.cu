@@ -433,13 +433,10 @@ __global__ void gram_reduce_kernel(const double* partial, long long num_blocks, 
 template <int NB, int OP>
 static cudaError_t launch_gram_nb(const GramParams& prm, long long num_blocks, cudaStream_t stream) {
   using Cfg = GramCfg<NB, OP>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gram_mma_kernel<NB, OP>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(Cfg::kSmemBytes));
+  static unsigned long long smem_ready = 0;  // per-device opt-in mask
+  {
+    cudaError_t e = opt_in_dynamic_smem(gram_mma_kernel<NB, OP>, Cfg::kSmemBytes, &smem_ready);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   gram_mma_kernel<NB, OP>
       <<<static_cast<unsigned>(num_blocks), Cfg::NW * kWarp, Cfg::kSmemBytes, stream>>>(prm);

@@ -599,12 +599,10 @@ cudaError_t launch_gram_wide(const MatView& x, long long m, int n, int sm_count,
   if (prm.kb_full > panels) prm.kb_full = static_cast<int>(panels > 0 ? panels : 1);
   if (prm.nchunk == 1) grid = prm.kb_tri; else grid = 2 * prm.kb_tri + prm.kb_full;
   const size_t bytes = sizeof(double) * kWStages * (kWC * kTriP > 2 * kWC * kFullP ? kWC * kTriP : 2 * kWC * kFullP);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gram_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(bytes));
+  static unsigned long long smem_ready = 0;  // per-device opt-in mask
+  {
+    cudaError_t e = opt_in_dynamic_smem(gram_wide_kernel, bytes, &smem_ready);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   gram_wide_kernel<<<grid, kWThreads, bytes, stream>>>(prm);
   cudaError_t e = cudaGetLastError();
@@ -619,25 +617,21 @@ size_t gram_wide_fused_scratch_doubles() { return fused_frag_doubles(OP_MULTIPLY
 template <int OP, bool WRITEQ = false>
 static cudaError_t launch_fused(const WideSolveParams& prm, cudaStream_t stream) {
   const size_t bytes = sizeof(double) * fused_smem_doubles(OP);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gram_wide_fused_kernel<OP, WRITEQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(bytes));
+  static unsigned long long smem_ready = 0;  // per-device opt-in mask
+  {
+    cudaError_t e = opt_in_dynamic_smem(gram_wide_fused_kernel<OP, WRITEQ>, bytes, &smem_ready);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   gram_wide_fused_kernel<OP, WRITEQ><<<prm.kb, kWThreads, bytes, stream>>>(prm);
   return cudaGetLastError();
 }
 
 static cudaError_t launch_rinv_wide(const double* r, int n, double* frags, StatusWord* status, cudaStream_t stream) {
-  static bool configured = false;
   const size_t rinv_bytes = sizeof(double) * (tri_size(kWC) + kWC * kWC);
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(rinv_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(rinv_bytes));
+  static unsigned long long smem_ready = 0;  // per-device opt-in mask
+  {
+    cudaError_t e = opt_in_dynamic_smem(rinv_wide_kernel, rinv_bytes, &smem_ready);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   rinv_wide_kernel<<<1, 128, rinv_bytes, stream>>>(r, n, frags, status);
   return cudaGetLastError();

@@ -3,11 +3,11 @@
 
 #include <cuda_runtime.h>
 
-#include "tsqr_warp.cuh"
+#include "warp_pipe.cuh"
 
 namespace sqb {
 
-// ---- tsqr_kernels.cu ---------------------------------------------------------------------
+// ---- TSQR streaming kernels ------------------------------------------------------------------
 struct TsqrParams {
   MatView x;
   long long m;
@@ -18,22 +18,14 @@ struct TsqrParams {
   int finalize;      // sign-normalise (reference sign_normalize, src/types.cpp:8-14)
   int check_finite;  // raise StatusWord::nonfinite when an Inf/NaN is streamed
   StatusWord* status;
-  int tune = 0;      // experiment switches (SQB_FOLD_TUNE), 0 in production
+  int kind = -1;     // kernel family (TsqrKind); -1 = the measured selection table
 };
-cudaError_t launch_tsqr_warp(const TsqrParams& prm, long long num_blocks, cudaStream_t stream);
-int tsqr_warp_panel_rows(int n);
-int tsqr_warp_warps(int n);
 
 // ---- tsqr_thread_kernels.cu (n <= 16: every thread is a leaf of the reduction tree) --------
 constexpr int kThreadTsqrMaxN = 16;
 cudaError_t launch_tsqr_thread(const TsqrParams& prm, long long num_blocks, cudaStream_t stream);
 int tsqr_thread_chunk_rows(int n);
 int tsqr_thread_warps(int n);
-
-// ---- tsqr_group_kernels.cu (8 < n <= 64: a group of G lanes is a leaf of the tree) ---------
-cudaError_t launch_tsqr_group(const TsqrParams& prm, long long num_blocks, cudaStream_t stream);
-int tsqr_group_chunk_rows(int n);
-int tsqr_group_warps(int n);
 
 // ---- tsqr_fold_kernels.cu (5 <= n <= 64: lookahead lane-group kernel with retire loads) -------
 constexpr int kFoldTsqrMinN = 5;
@@ -48,52 +40,37 @@ int tsqr_mma_panel_rows(int n);
 int tsqr_mma_warps(int n);
 
 // Kernel selection by column count (measured on B200, profiles/README.md): register-resident thread
-// kernel up to 4 columns, lookahead fold kernel for 5..28, DMMA blocked kernel for 29..64.
-// SQB_TSQR_KERNEL=0..4 forces thread / lane-group / warp-panel / fold / DMMA where the column count
-// allows it (tuning, A/B tests and the kernel-family parity test only).
-int tsqr_forced_kind();
-inline int tsqr_kernel_kind(int n) {
-  const int f = tsqr_forced_kind();
-  if (f == 0 && n <= kThreadTsqrMaxN) return 0;
-  if (f == 1 && n > 8) return 1;
-  if (f == 2) return 2;
-  if (f == 3 && n >= kFoldTsqrMinN) return 3;
-  if (f == 4 && n >= kMmaTsqrMinN) return 4;
-  if (f >= 0 && f <= 4) {  // forced kind not available for this n: fall back to the legacy table
-    if (n <= 14) return 0;
-    if (n <= 24) return 1;
-    if (n <= 32) return 2;
-    return 1;
-  }
-  if (n < kFoldTsqrMinN) return 0;
-  if (n <= 28) return 3;
-  return 4;
+// kernel up to 4 columns, lookahead fold kernel for 5..28, DMMA blocked kernel for 29..64.  A
+// context may force one family where the column count allows it (sqb_set_tsqr_kernel: A/B timing
+// and the kernel-family parity test); a family that cannot run this n falls back to the table.
+enum TsqrKind { kTsqrAuto = -1, kTsqrThread = 0, kTsqrFold = 1, kTsqrMma = 2 };
+inline int tsqr_kernel_kind(int n, int forced) {
+  if (forced == kTsqrThread && n <= kThreadTsqrMaxN) return kTsqrThread;
+  if (forced == kTsqrFold && n >= kFoldTsqrMinN) return kTsqrFold;
+  if (forced == kTsqrMma && n >= kMmaTsqrMinN) return kTsqrMma;
+  if (n < kFoldTsqrMinN) return kTsqrThread;
+  if (n <= 28) return kTsqrFold;
+  return kTsqrMma;
 }
 inline cudaError_t launch_tsqr_any(const TsqrParams& prm, long long num_blocks, cudaStream_t stream) {
-  switch (tsqr_kernel_kind(prm.n)) {
-    case 0: return launch_tsqr_thread(prm, num_blocks, stream);
-    case 1: return launch_tsqr_group(prm, num_blocks, stream);
-    case 3: return launch_tsqr_fold(prm, num_blocks, stream);
-    case 4: return launch_tsqr_mma(prm, num_blocks, stream);
-    default: return launch_tsqr_warp(prm, num_blocks, stream);
+  switch (tsqr_kernel_kind(prm.n, prm.kind)) {
+    case kTsqrThread: return launch_tsqr_thread(prm, num_blocks, stream);
+    case kTsqrFold: return launch_tsqr_fold(prm, num_blocks, stream);
+    default: return launch_tsqr_mma(prm, num_blocks, stream);
   }
 }
-inline int tsqr_panel_rows(int n) {
-  switch (tsqr_kernel_kind(n)) {
-    case 0: return tsqr_thread_chunk_rows(n);
-    case 1: return tsqr_group_chunk_rows(n);
-    case 3: return tsqr_fold_chunk_rows(n);
-    case 4: return tsqr_mma_panel_rows(n);
-    default: return tsqr_warp_panel_rows(n);
+inline int tsqr_panel_rows(int n, int forced) {
+  switch (tsqr_kernel_kind(n, forced)) {
+    case kTsqrThread: return tsqr_thread_chunk_rows(n);
+    case kTsqrFold: return tsqr_fold_chunk_rows(n);
+    default: return tsqr_mma_panel_rows(n);
   }
 }
-inline int tsqr_warps(int n) {
-  switch (tsqr_kernel_kind(n)) {
-    case 0: return tsqr_thread_warps(n);
-    case 1: return tsqr_group_warps(n);
-    case 3: return tsqr_fold_warps(n);
-    case 4: return tsqr_mma_warps(n);
-    default: return tsqr_warp_warps(n);
+inline int tsqr_warps(int n, int forced) {
+  switch (tsqr_kernel_kind(n, forced)) {
+    case kTsqrThread: return tsqr_thread_warps(n);
+    case kTsqrFold: return tsqr_fold_warps(n);
+    default: return tsqr_mma_warps(n);
   }
 }
 

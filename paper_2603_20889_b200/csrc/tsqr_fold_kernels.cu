@@ -7,7 +7,7 @@
 // packed triangle in shared memory; lane g of the group keeps columns g, g+G, g+2G, ... of those
 // rows in registers (w[slot][row]).
 //
-// What is new against tsqr_group_kernels.cu / tsqr_thread_kernels.cu (both FP64-latency bound):
+// What is new against tsqr_thread_kernels.cu (FP64-latency bound beyond a handful of columns):
 //   * LOOKAHEAD: step c first applies reflector c to the slot that holds column c+1, then derives
 //     reflector c+1 (norm, sqrt, reciprocal - a ~15-instruction dependent chain) while the
 //     remaining slots are still being updated with reflector c.  Both live in one basic block, so
@@ -18,7 +18,6 @@
 //   * G = 1 (thread-private leaves, no shuffles at all) up to n = 16 with 6-8 rows per step.
 // Per reflector the only communication is the broadcast of the P-entry reflector column from its
 // owner lane (P 64-bit shuffles inside the group, none for G = 1); every dot product is lane-local.
-#include <cstdlib>
 #include <type_traits>
 
 #include "kernels.h"
@@ -248,7 +247,7 @@ __global__ void __launch_bounds__(FoldCfg<NS, G, P, TMAX>::T, 1) tsqr_fold_kerne
     }
     const long long rn = r0 + static_cast<long long>(NW) * CH;  // the warp's next chunk
     const bool fast = aligned && rn + CH <= end;
-    if (fast && !(prm.tune & 1) && rn + static_cast<long long>(NW + 1) * CH <= end) {
+    if (fast && rn + static_cast<long long>(NW + 1) * CH <= end) {
       // pull the chunk after the next one towards L2
       for (int j = lane; j < n; j += 32) {
         const double* nxt = prm.x.col(j) + rn + static_cast<long long>(NW) * CH;
@@ -308,13 +307,10 @@ __global__ void __launch_bounds__(FoldCfg<NS, G, P, TMAX>::T, 1) tsqr_fold_kerne
 template <int NS, int G, int P, int TMAX>
 cudaError_t launch_cfg(const TsqrParams& prm, long long num_blocks, cudaStream_t stream) {
   using Cfg = FoldCfg<NS, G, P, TMAX>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(tsqr_fold_kernel<NS, G, P, TMAX>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(Cfg::kSmemBytes));
+  static unsigned long long smem_ready = 0;  // per-device opt-in mask
+  {
+    cudaError_t e = opt_in_dynamic_smem(tsqr_fold_kernel<NS, G, P, TMAX>, Cfg::kSmemBytes, &smem_ready);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   tsqr_fold_kernel<NS, G, P, TMAX>
       <<<static_cast<unsigned>(num_blocks), Cfg::T, Cfg::kSmemBytes, stream>>>(prm);
@@ -327,7 +323,7 @@ cudaError_t launch_cfg(const TsqrParams& prm, long long num_blocks, cudaStream_t
 // on B200 (gpurun_out/fold_select.txt, profiles/README.md): thread-private leaves up to 14 columns
 // (5..8 columns: taller steps than the register-triangle kernel, 5-9 % faster under the power cap),
 // lane pairs up to 20, lane quads up to 28; above that the DMMA kernel (tsqr_mma_kernels.cu) wins
-// and the last three rows only serve SQB_TSQR_KERNEL=3
+// and the last three rows only serve a forced kernel family (sqb_set_tsqr_kernel)
 #define SQB_FOLD_SWITCH(EXPR)                 \
   switch (n) {                                \
     case 5: return EXPR(5, 1, 16, 256);       \
@@ -351,63 +347,22 @@ cudaError_t launch_cfg(const TsqrParams& prm, long long num_blocks, cudaStream_t
   if (n <= 48) return EXPR(3, 16, 16, 256);   \
   return EXPR(4, 16, 16, 256);
 
-#ifdef SQB_FOLD_EXPERIMENT
-static int fold_variant() {
-  static int v = [] { const char* e = getenv("SQB_FOLD_VARIANT"); return e ? atoi(e) : 0; }();
-  return v;
-}
-#define SQB_FOLD_EXPERIMENTS(EXPR)                                                        \
-  {                                                                                       \
-    const int v = fold_variant();                                                         \
-    const int h = (n + 1) / 2;                                                            \
-    if (v == 1 && n <= 24) switch (h) {                                                   \
-        case 5: return EXPR(5, 2, 8, 256); case 6: return EXPR(6, 2, 8, 256); case 7: return EXPR(7, 2, 8, 256); \
-        case 8: return EXPR(8, 2, 8, 256); case 9: return EXPR(9, 2, 8, 256); case 10: return EXPR(10, 2, 8, 256); \
-        case 11: return EXPR(11, 2, 8, 256); case 12: return EXPR(12, 2, 8, 256); default: break; }     \
-    if (v == 2 && n <= 20) switch (h) {                                                   \
-        case 5: return EXPR(5, 2, 12, 256); case 6: return EXPR(6, 2, 12, 256); case 7: return EXPR(7, 2, 12, 256); \
-        case 8: return EXPR(8, 2, 12, 256); case 9: return EXPR(9, 2, 12, 256); case 10: return EXPR(10, 2, 12, 256); \
-        default: break; }                                                                 \
-    if (v == 3 && n <= 16) switch (h) {                                                   \
-        case 5: return EXPR(5, 2, 16, 256); case 6: return EXPR(6, 2, 16, 256); case 7: return EXPR(7, 2, 16, 256); \
-        case 8: return EXPR(8, 2, 16, 256); default: break; }                             \
-    if (v == 4 && n > 16 && n <= 32) { const int f = (n + 3) / 4; switch (f) {            \
-        case 5: return EXPR(5, 4, 12, 256); case 6: return EXPR(6, 4, 12, 256); case 7: return EXPR(7, 4, 12, 256); \
-        case 8: return EXPR(8, 4, 12, 256); default: break; } }                           \
-    if (v == 5 && n > 16 && n <= 32) { const int f = (n + 3) / 4; switch (f) {            \
-        case 5: return EXPR(5, 4, 16, 256); case 6: return EXPR(6, 4, 16, 256); case 7: return EXPR(7, 4, 8, 256); \
-        case 8: return EXPR(8, 4, 8, 256); default: break; } }                            \
-  }
-#else
-#define SQB_FOLD_EXPERIMENTS(EXPR)
-#endif
-
-static int fold_tune() {
-  static int v = [] { const char* e = getenv("SQB_FOLD_TUNE"); return e ? atoi(e) : 0; }();
-  return v;
-}
-
-cudaError_t launch_tsqr_fold(const TsqrParams& prm_in, long long num_blocks, cudaStream_t stream) {
-  TsqrParams prm = prm_in;
-  prm.tune = fold_tune();
+cudaError_t launch_tsqr_fold(const TsqrParams& prm, long long num_blocks, cudaStream_t stream) {
   const int n = prm.n;
   if (n < kFoldTsqrMinN || n > 64) return cudaErrorInvalidValue;
 #define LG(NSV, GV, PV, TV) launch_cfg<NSV, GV, PV, TV>(prm, num_blocks, stream)
-  SQB_FOLD_EXPERIMENTS(LG)
   SQB_FOLD_SWITCH(LG)
 #undef LG
 }
 
 int tsqr_fold_chunk_rows(int n) {
 #define CG(NSV, GV, PV, TV) FoldCfg<NSV, GV, PV, TV>::kChunk
-  SQB_FOLD_EXPERIMENTS(CG)
   SQB_FOLD_SWITCH(CG)
 #undef CG
 }
 
 int tsqr_fold_warps(int n) {
 #define WG(NSV, GV, PV, TV) (FoldCfg<NSV, GV, PV, TV>::T / 32)
-  SQB_FOLD_EXPERIMENTS(WG)
   SQB_FOLD_SWITCH(WG)
 #undef WG
 }

@@ -335,13 +335,10 @@ __global__ void __launch_bounds__(NW * 32, 1) tsqr_mma_kernel(const TsqrParams p
 template <int NB, int RG, int NW>
 cudaError_t launch_cfg(const TsqrParams& prm, long long num_blocks, cudaStream_t stream) {
   using Cfg = MmaCfg<NB, RG, NW>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(tsqr_mma_kernel<NB, RG, NW>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(Cfg::kSmemBytes));
+  static unsigned long long smem_ready = 0;  // per-device opt-in mask
+  {
+    cudaError_t e = opt_in_dynamic_smem(tsqr_mma_kernel<NB, RG, NW>, Cfg::kSmemBytes, &smem_ready);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   tsqr_mma_kernel<NB, RG, NW><<<static_cast<unsigned>(num_blocks), Cfg::T, Cfg::kSmemBytes, stream>>>(prm);
   return cudaGetLastError();

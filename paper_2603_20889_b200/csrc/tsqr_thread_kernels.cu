@@ -196,15 +196,10 @@ __global__ void __launch_bounds__(ThreadCfg<N>::T, 1) tsqr_thread_kernel(const T
 template <int N>
 cudaError_t launch_n(const TsqrParams& prm, long long num_blocks, cudaStream_t stream) {
   using Cfg = ThreadCfg<N>;
-  static bool configured = false;
-  if (!configured) {
-    if (Cfg::kSmemBytes > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(tsqr_thread_kernel<N>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(Cfg::kSmemBytes));
-      if (e != cudaSuccess) return e;
-    }
-    configured = true;
+  static unsigned long long smem_ready = 0;  // per-device opt-in mask
+  {
+    cudaError_t e = opt_in_dynamic_smem(tsqr_thread_kernel<N>, Cfg::kSmemBytes, &smem_ready);
+    if (e != cudaSuccess) return e;
   }
   tsqr_thread_kernel<N><<<static_cast<unsigned>(num_blocks), Cfg::T, Cfg::kSmemBytes, stream>>>(prm);
   return cudaGetLastError();

@@ -62,6 +62,29 @@ __device__ __forceinline__ bool issue_panel(const MatView& x, int n, long long r
   return false;
 }
 
+// Running triangle of the TSQR kernels: packed ROW-major upper triangle of order npad; row c holds
+// (c, c..npad-1).  row_base(c) + j addresses entry (c, j); consecutive rows differ by npad - c - 1,
+// so a factorisation walks it with one running offset and no index multiplications.
+__host__ __device__ __forceinline__ int row_base(int c, int npad) {
+  return c * npad - (c * (c - 1)) / 2 - c;
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-DEVICE attribute: opt in once per device
+// (a process may hold contexts on several GPUs), remembered in a per-kernel bit mask.
+template <class Kernel>
+inline cudaError_t opt_in_dynamic_smem(Kernel kernel, size_t bytes, unsigned long long* done_mask) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 64 && ((*done_mask >> dev) & 1ull)) return cudaSuccess;
+  if (bytes > 48 * 1024) {
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    if (e != cudaSuccess) return e;
+  }
+  if (dev < 64) *done_mask |= 1ull << dev;
+  return cudaSuccess;
+}
+
 // Fused non-finite validation (replaces the reference's serial scans, src/types.cpp:40-48 and
 // src/gram.cpp:96-102): an Inf/NaN anywhere in X makes the squared norm of its column - hence the
 // diagonal of R or of the Gram matrix - non-finite, so testing the n x n result is enough.

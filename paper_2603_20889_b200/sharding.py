@@ -1,19 +1,29 @@
-"""Row-sharded (multi-GPU) orchestration: one process per GPU, rows split into contiguous slabs,
-only n x n matrices cross the interconnect.
+"""Host-side wiring of the row-sharded (multi-GPU) runs: one process per GPU, rows split into
+contiguous slabs, only n x n matrices cross the interconnect.
 
-The reference has no distributed code; this is its k-block structure one level up
+The reference has no distributed code; the protocol is its k-block structure one level up
 (reference src/tsqr.cpp:175-195: k block triangles stacked into Y, one more block QR of Y;
-src/gram.cpp:81-92: block partials summed).  Two interchangeable transports exist:
+src/gram.cpp:81-92: block partials summed in ascending order) and it is implemented ONCE, in the
+C library (``sqb_*_sharded_dev``: local pass -> all-gather of n x n blocks -> combine kernels).
+This module only provides what a launcher needs around it - nothing here computes:
 
-* the C ABI's ``sqb_*_sharded_dev`` entry points (NCCL resolved inside libskinnyqr_b200.so), used by
-  ``bench.py``;
-* the functions below, which run the same exchange through ``torch.distributed`` (NCCL on GPUs,
-  gloo in the CPU tests) around pluggable local kernels.  The local kernels are always supplied by
-  the caller - on a GPU box they are the CUDA entry points of ``Context``; nothing here computes.
+* ``slab_bounds``      which rows a rank owns;
+* ``attach``           gives a ``Context`` its transport: NCCL inside the library (communicator
+                       id broadcast through ``torch.distributed``) when the process group runs on
+                       NCCL, otherwise ``TorchExchange``;
+* ``TorchExchange``    the library's all-gather hook (``sqb_set_allgather``) served by any
+                       ``torch.distributed`` backend through host staging - this is how the C
+                       drivers are exercised with world > 1 on one GPU (gloo) and how an MPI-style
+                       host transport would plug in;
+* ``max_over_ranks``   the bench's timing reduction.
+
+``bench.py`` and the multi-rank tests use exactly these functions.
 """
 from __future__ import annotations
 
-from typing import Callable, Tuple
+from typing import Tuple
+
+import numpy as np
 
 
 def slab_bounds(m: int, world: int, rank: int) -> Tuple[int, int]:
@@ -26,36 +36,78 @@ def slab_bounds(m: int, world: int, rank: int) -> Tuple[int, int]:
     return min(rank * per, m), min((rank + 1) * per, m)
 
 
-def tsqr_qless_sharded(x_local, local_qr: Callable, stack_qr: Callable, dist, group=None):
-    """R of the row-sharded matrix whose slab on this rank is `x_local` (m_local x n).
-
-    local_qr(x_local) -> n x n un-normalised triangle of the slab (zeros for an empty slab);
-    stack_qr(y)       -> sign-normalised triangle of the (world*n) x n stack of triangles.
-    Every rank returns the same R (all-gather + redundant final combine)."""
+def _backend_device(dist, group=None):
+    """Tensors handed to the collectives of this process group live on this device."""
     import torch
-
-    r_local = local_qr(x_local)
-    world = dist.get_world_size(group)
-    n = r_local.shape[0]
-    pieces = [torch.empty_like(r_local) for _ in range(world)]
-    dist.all_gather(pieces, r_local.contiguous(), group=group)
-    y = torch.cat([p.reshape(n, n) for p in pieces], dim=0)  # rank g's triangle at rows [g*n, g*n+n)
-    return stack_qr(y)
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
 
 
-def gram_sharded(x_local, local_gram: Callable, dist, group=None):
-    """Sum over ranks of the slab Gram matrices (all-reduce of n*n doubles)."""
-    c = local_gram(x_local).contiguous()
-    dist.all_reduce(c, op=dist.ReduceOp.SUM, group=group)
-    return c
+def broadcast_bytes(payload, dist, src=0, group=None) -> bytes:
+    """`payload` (bytes on rank `src`, ignored elsewhere) -> the same bytes on every rank."""
+    box = [payload if dist.get_rank(group) == src else None]
+    dist.broadcast_object_list(box, src=src, group=group)
+    return bytes(box[0])
 
 
-def cholqr2_sharded(x_local, gram: Callable, gram_solve: Callable, cholesky: Callable,
-                    tri_multiply: Callable, dist, group=None):
-    """Cholesky-QR2 over row slabs: two streaming passes, two all-reduces, factorisations replicated
-    on every rank (reference gram_qr.cpp:123-131)."""
-    c1 = gram_sharded(x_local, gram, dist, group)
-    r1 = cholesky(c1)
-    c2 = gram_sharded(x_local, lambda xl: gram_solve(xl, r1), dist, group)
-    r2 = cholesky(c2)
-    return tri_multiply(r2, r1)
+def max_over_ranks(value: float, dist, group=None) -> float:
+    """Slowest rank's figure (bench contract: device time, max over ranks)."""
+    import torch
+    if dist is None or not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=_backend_device(dist, group))
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
+class TorchExchange:
+    """All-gather of `count` doubles per rank through torch.distributed.
+
+    ``gather_host`` is the transport proper (host arrays in, host array out); ``__call__`` is the
+    signature the library's hook expects (device addresses): it stages through host memory with
+    the context's stream-ordered copies, so the gathered blocks are valid for everything the
+    library enqueues afterwards."""
+
+    def __init__(self, dist, group=None, ctx=None):
+        self.dist, self.group, self.ctx = dist, group, ctx
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.calls = 0
+
+    def gather_host(self, block: np.ndarray) -> np.ndarray:
+        """(count,) float64 on every rank -> (world, count): row g is rank g's block."""
+        import torch
+        dev = _backend_device(self.dist, self.group)
+        send = torch.from_numpy(np.ascontiguousarray(block, dtype=np.float64)).to(dev)
+        pieces = [torch.empty_like(send) for _ in range(self.world)]
+        self.dist.all_gather(pieces, send, group=self.group)
+        self.calls += 1
+        return torch.stack(pieces).cpu().numpy()
+
+    def __call__(self, send_ptr: int, recv_ptr: int, count: int) -> int:
+        send = np.empty(count, dtype=np.float64)
+        self.ctx.copy_d2h(send, send_ptr)
+        gathered = np.ascontiguousarray(self.gather_host(send))
+        self.ctx.copy_h2d(recv_ptr, gathered)
+        return 0
+
+
+def attach(ctx, dist, group=None, transport: str = "auto"):
+    """Make `ctx` a member of the process group: afterwards ``ctx.*_sharded`` run over all ranks.
+
+    transport "nccl": the library's own NCCL communicator (rank 0 creates the unique id, it is
+    broadcast through the process group); "torch": ``TorchExchange`` over whatever backend the
+    group uses; "auto": NCCL when the group itself runs on NCCL.  Returns the transport's name."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    if transport == "auto":
+        transport = "nccl" if dist.get_backend(group) == "nccl" else "torch"
+    if transport == "nccl":
+        uid = broadcast_bytes(ctx.nccl_unique_id() if rank == 0 else None, dist, 0, group)
+        ctx.init_nccl(uid, rank, world)
+    elif transport == "torch":
+        ctx.exchange = TorchExchange(dist, group, ctx)
+        ctx.set_allgather(ctx.exchange, rank, world)
+    else:
+        raise ValueError(f"unknown transport {transport!r}")
+    return transport

@@ -1,6 +1,9 @@
-"""N > 1 host logic on CPU: two gloo ranks, row slabs, all-gather of triangles / all-reduce of Gram
-matrices through paper_2603_20889_b200.sharding.  The per-slab kernels are stood in for by the CPU
-oracle (test infrastructure); what is under test is the exchange and the combine wiring."""
+"""N > 1 host logic on CPU: two gloo ranks driving paper_2603_20889_b200.sharding - the same
+functions bench.py and the multi-rank GPU test use (slab_bounds, broadcast_bytes, max_over_ranks,
+TorchExchange.gather_host).  The protocol itself lives in the C library (sqb_*_sharded_dev) and is
+covered at world > 1 by tests/test_sharded_gpu.py; here its host side is replayed with the CPU oracle
+standing in for the per-slab kernels (test infrastructure), in the library's order: local triangle ->
+all-gather -> stack -> one more block QR; local Gram -> all-gather -> ascending-rank sum."""
 import os
 import socket
 import sys
@@ -19,7 +22,6 @@ def _free_port():
 
 
 def _worker(rank, world, port, m, n, out_dir):
-    import torch
     import torch.distributed as dist
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "tests"))
@@ -28,32 +30,40 @@ def _worker(rank, world, port, m, n, out_dir):
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    ex = sharding.TorchExchange(dist)
+    assert (ex.rank, ex.world) == (rank, world)
+
+    # launcher helpers
+    uid = sharding.broadcast_bytes(bytes(range(128)) if rank == 0 else None, dist)
+    assert uid == bytes(range(128))
+    assert sharding.max_over_ranks(1.0 + rank, dist) == float(world)
+    g = ex.gather_host(np.full(3, float(rank)))
+    assert g.shape == (world, 3) and np.array_equal(g[:, 0], np.arange(world, dtype=np.float64))
+
     x = oracle.gaussian(m, n, 99)
     lo, hi = sharding.slab_bounds(m, world, rank)
-    xl = torch.from_numpy(np.ascontiguousarray(x[lo:hi]))
+    xl = np.asfortranarray(x[lo:hi])
 
-    def to_np(t):
-        return np.asfortranarray(t.numpy())
+    # TSQR: stage 2 with k = world (tsqr.cpp:175-195)
+    r_local = oracle.port.block_qless_qr(xl, 64) if hi > lo else np.zeros((n, n), order="F")
+    gathered = ex.gather_host(np.asfortranarray(r_local).ravel(order="F"))
+    stack = np.asfortranarray(np.concatenate([blk.reshape(n, n, order="F") for blk in gathered], axis=0))
+    r = oracle.port.tsqr_qless(stack, 1, stack.shape[0])
 
-    def local_qr(t):
-        if t.shape[0] == 0:
-            return torch.zeros((n, n), dtype=torch.float64)
-        return torch.from_numpy(np.ascontiguousarray(oracle.port.block_qless_qr(to_np(t), 64)))
+    # CholQR2: every Gram partial all-gathered and summed in ascending rank order (gram.cpp:81-92)
+    def allsum(c):
+        parts = ex.gather_host(np.asfortranarray(c).ravel(order="F"))
+        acc = parts[0].copy()
+        for blk in parts[1:]:
+            acc += blk
+        return np.asfortranarray(acc.reshape(n, n, order="F"))
 
-    def stack_qr(y):
-        yy = to_np(y)
-        return torch.from_numpy(np.ascontiguousarray(oracle.port.tsqr_qless(yy, 1, yy.shape[0])))
-
-    r = sharding.tsqr_qless_sharded(xl, local_qr, stack_qr, dist)
-    rc = sharding.cholqr2_sharded(
-        xl,
-        lambda t: torch.from_numpy(np.ascontiguousarray(oracle.port.tsmttsm(to_np(t), 1, 64))),
-        lambda t, r1: torch.from_numpy(np.ascontiguousarray(oracle.port.tsmRttsmR(to_np(t), to_np(r1), 1, 64))),
-        lambda c: torch.from_numpy(np.ascontiguousarray(oracle.port.cholesky(to_np(c)))),
-        lambda a, b: torch.from_numpy(np.ascontiguousarray(oracle.port.triangular_multiply(to_np(a), to_np(b)))),
-        dist)
-    np.save(Path(out_dir) / f"r_{rank}.npy", r.numpy())
-    np.save(Path(out_dir) / f"rc_{rank}.npy", rc.numpy())
+    zero = np.zeros((n, n), order="F")
+    r1 = oracle.port.cholesky(allsum(oracle.port.tsmttsm(xl, 1, 64) if hi > lo else zero))
+    r2 = oracle.port.cholesky(allsum(oracle.port.tsmRttsmR(xl, r1, 1, 64) if hi > lo else zero))
+    rc = oracle.port.triangular_multiply(r2, r1)
+    np.save(Path(out_dir) / f"r_{rank}.npy", r)
+    np.save(Path(out_dir) / f"rc_{rank}.npy", rc)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -74,3 +84,24 @@ def test_two_rank_combine_matches_single_process(tmp_path, m, n):
     rc0, rc1 = np.load(tmp_path / "rc_0.npy"), np.load(tmp_path / "rc_1.npy")
     assert np.array_equal(rc0, rc1)
     assert np.linalg.norm(rc0 - r_ref) <= bound
+
+
+def test_slab_bounds_cover_rows_once():
+    from paper_2603_20889_b200 import sharding
+    for m, world in [(0, 3), (5, 8), (1000, 7), (2**27, 8), (10**9, 8)]:
+        cuts = [sharding.slab_bounds(m, world, g) for g in range(world)]
+        assert cuts[0][0] == 0 and cuts[-1][1] == m
+        assert all(a[1] == b[0] for a, b in zip(cuts, cuts[1:]))
+        assert all(lo <= hi for lo, hi in cuts)
+    with pytest.raises(ValueError):
+        sharding.slab_bounds(10, 2, 2)
+
+
+def test_bench_spawn_command():
+    """bench.py --gpus N (no torchrun around it) re-executes itself under torch.distributed.run."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    cmd = bench.spawn_command(4, ["--gpus", "4", "--steps", "5"], port=29999)
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd and "--master-port=29999" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "5"] and cmd[-5].endswith("bench.py")
