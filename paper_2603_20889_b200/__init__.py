@@ -277,16 +277,20 @@ class Context:
         return PanelPlan(int(k.value), int(b.value), True)
 
     # -- device-side helpers (torch tensors are only memory handles here)
-    def _dev(self, t):
-        import torch
-        if t.dtype != torch.float64 or not t.is_cuda:
-            raise ArgumentError("device inputs must be float64 CUDA tensors")
+    def _follow_torch_stream(self):
         # device tensors are produced by torch kernels on torch's current stream: enqueue behind them
-        # (an own stream would race with the producer of `t`); host-pointer calls keep the own stream
+        # (an own stream would race with the producer); host-pointer calls keep the own stream
+        import torch
         cur = torch.cuda.current_stream(self.device).cuda_stream
         if cur != self._torch_stream:
             self.set_stream(cur)
             self._torch_stream = cur
+
+    def _dev(self, t):
+        import torch
+        if t.dtype != torch.float64 or not t.is_cuda:
+            raise ArgumentError("device inputs must be float64 CUDA tensors")
+        self._follow_torch_stream()
         if t.dim() == 1:
             return C.c_void_p(t.data_ptr()), t.shape[0], 1, max(t.shape[0], 1)
         m, n = t.shape
@@ -596,7 +600,7 @@ class Context:
             raise DimensionError(f"{what}: expected world contiguous n x n blocks")
         if g.dtype != torch.float64 or not g.is_cuda or g.device.index != self.device:
             raise ArgumentError(f"{what}: blocks must be float64 CUDA tensors on this device")
-        self._dev(g[0])  # stream bookkeeping
+        self._follow_torch_stream()
         return g, g.shape[0], g.shape[1]
 
     def tsqr_combine(self, blocks):
