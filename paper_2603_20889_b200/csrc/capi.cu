@@ -215,7 +215,18 @@ int gram_wide_view(sqb_context* ctx, const MatView& v, long long m, int n, int o
     ctx->launches += 2;
     return SQB_OK;
   }
-  if (n > kWideFusedMaxN) return SQB_E_ARGUMENT;
+  if (n > kWideGramMaxN) return SQB_E_ARGUMENT;
+  if (n > kWideFusedMaxN) {
+    // 129..256 columns: Q = X F per row slab (128 x 128 factor blocks), wide SYRK on the slab
+    const size_t sc = gram_wide2_scratch_doubles(n), nn = static_cast<size_t>(n) * n;
+    SQB_TRY(grow(&ctx->work, &ctx->work_doubles, partial + sc + nn));
+    const long long slab_rows = std::min<long long>((std::max<long long>(m, 8) + 7) / 8 * 8, 1ll << 20);
+    SQB_TRY(grow(&ctx->qslab, &ctx->qslab_doubles, static_cast<size_t>(slab_rows) * n));
+    SQB_CUDA(launch_gram_wide2_fused(v, m, n, op, factor, ctx->sm_count, ctx->work + partial, ctx->qslab, slab_rows,
+                                     ctx->work, ctx->work + partial + sc, d_c, ctx->d_status, ctx->stream,
+                                     &ctx->launches));
+    return SQB_OK;
+  }
   SQB_TRY(grow(&ctx->work, &ctx->work_doubles, partial + gram_wide_fused_scratch_doubles()));
   SQB_CUDA(launch_gram_wide_fused(v, m, n, op, factor, ctx->sm_count, ctx->work + partial, ctx->work, d_c,
                                   ctx->d_status, ctx->stream));
@@ -544,6 +555,7 @@ int sqb_destroy(sqb_context* ctx) {
   cudaFree(ctx->small);
   cudaFree(ctx->xbuf);
   cudaFree(ctx->ring);
+  cudaFree(ctx->qslab);
   for (cudaEvent_t e : ctx->ring_free)
     if (e) cudaEventDestroy(e);
   cudaFree(ctx->gen);
@@ -687,7 +699,7 @@ static int gram_entry(sqb_context* ctx, const double* d_x, int64_t m, int64_t n,
   if (n < 1 || m < 0) return SQB_E_DIMENSION;
   if (ld < m) return SQB_E_ARGUMENT;
   if (op == OP_MULTIPLY) {  // tsmmttsmm checks B for finiteness at any n (gram.cpp:143-145)
-    if (n > kWideFusedMaxN) return SQB_E_ARGUMENT;
+    if (n > kWideGramMaxN) return SQB_E_ARGUMENT;
     SQB_CUDA(launch_check_finite(factor, n * n, ctx->d_status, ctx->stream));
     ctx->launches++;
   }
@@ -719,7 +731,7 @@ int sqb_tsmmttsmm_dev(sqb_context* ctx, const double* d_x, int64_t m, int64_t n,
 int sqb_cholesky_dev(sqb_context* ctx, const double* d_c, int64_t n, double* d_r) {
   SQB_TRY(enter(ctx));
   if (n < 1) return SQB_E_DIMENSION;
-  if (n > kSmallMaxN) return SQB_E_ARGUMENT;
+  if (n > kWideGramMaxN) return SQB_E_ARGUMENT;  // the reference has no limit (gram_qr.cpp:36-58); 256 = config 5
   SQB_CUDA(launch_cholesky(d_c, static_cast<int>(n), d_r, ctx->d_status, ctx->stream));
   ctx->launches++;
   return SQB_OK;
@@ -741,7 +753,7 @@ int sqb_eigh_small_dev(sqb_context* ctx, const double* d_c, int64_t n, double* d
 int sqb_cholqr2_dev(sqb_context* ctx, const double* d_x, int64_t m, int64_t n, int64_t ld,
                     int64_t num_blocks, int64_t panel_rows, double* d_r) {
   SQB_TRY(enter(ctx));
-  SQB_TRY(check_shape(m, n, ld, kWideFusedMaxN));
+  SQB_TRY(check_shape(m, n, ld, kWideGramMaxN));
   if (n > 64) return cholqr2_wide(ctx, plain_view(d_x, ld, static_cast<int>(n)), m, static_cast<int>(n), d_r, nullptr);
   return cholqr2_view(ctx, plain_view(d_x, ld, static_cast<int>(n)), m, static_cast<int>(n), num_blocks,
                       panel_rows, d_r, nullptr);
@@ -778,7 +790,14 @@ int sqb_reconstruct_q_dev(sqb_context* ctx, const double* d_x, int64_t m, int64_
                           const double* d_r, double* d_q, int64_t ldq) {
   SQB_TRY(enter(ctx));
   if (n < 1 || m < 0) return SQB_E_DIMENSION;
-  if (n > kWideFusedMaxN || ld < m || ldq < m) return SQB_E_ARGUMENT;
+  if (n > kWideGramMaxN || ld < m || ldq < m) return SQB_E_ARGUMENT;
+  if (n > kWideFusedMaxN) {
+    SQB_TRY(grow(&ctx->work, &ctx->work_doubles, gram_wide2_scratch_doubles(static_cast<int>(n))));
+    SQB_CUDA(launch_apply_rinv_wide2(d_x, m, static_cast<int>(n), ld, d_r, ctx->sm_count, ctx->work, d_q, ldq,
+                                     ctx->d_status, ctx->stream));
+    ctx->launches += 9;
+    return SQB_OK;
+  }
   if (n > 64) {
     SQB_TRY(grow(&ctx->work, &ctx->work_doubles, gram_wide_partial_doubles(static_cast<int>(n), ctx->sm_count) +
                                                      gram_wide_fused_scratch_doubles()));
@@ -964,7 +983,7 @@ static int gram_host(sqb_context* ctx, const double* x, int64_t m, int64_t n, in
                      const double* factor, int64_t k, int64_t b, double* c) {
   SQB_TRY(enter_host(ctx));
   if (n < 1 || m < 0) return SQB_E_DIMENSION;
-  if (n > (op == OP_PLAIN ? kWideGramMaxN : kWideFusedMaxN) || ld < m) return SQB_E_ARGUMENT;
+  if (n > kWideGramMaxN || ld < m) return SQB_E_ARGUMENT;
   const int nn = static_cast<int>(n);
   Small s;
   SQB_TRY(small_slots(ctx, nn, &s));
@@ -1017,7 +1036,7 @@ int sqb_tsmmttsmm_host(sqb_context* ctx, const double* x, int64_t m, int64_t n, 
 int sqb_cholesky_host(sqb_context* ctx, const double* c, int64_t n, double* r) {
   SQB_TRY(enter_host(ctx));
   if (n < 1) return SQB_E_DIMENSION;
-  if (n > kSmallMaxN) return SQB_E_ARGUMENT;
+  if (n > kWideGramMaxN) return SQB_E_ARGUMENT;
   Small s;
   SQB_TRY(small_slots(ctx, static_cast<int>(n), &s));
   SQB_TRY(upload_small(ctx, c, static_cast<size_t>(n) * n, s.c1));
@@ -1043,7 +1062,7 @@ int sqb_eigh_small_host(sqb_context* ctx, const double* c, int64_t n, double* va
 int sqb_cholqr2_host(sqb_context* ctx, const double* x, int64_t m, int64_t n, int64_t ld,
                      int64_t num_blocks, int64_t panel_rows, double* r) {
   SQB_TRY(enter_host(ctx));
-  SQB_TRY(check_shape(m, n, ld, kWideFusedMaxN));
+  SQB_TRY(check_shape(m, n, ld, kWideGramMaxN));
   const int nn = static_cast<int>(n);
   Small s;
   SQB_TRY(small_slots(ctx, nn, &s));
@@ -1098,7 +1117,7 @@ int sqb_reconstruct_q_host(sqb_context* ctx, const double* x, int64_t m, int64_t
                            const double* r, double* q, int64_t ldq) {
   SQB_TRY(enter_host(ctx));
   if (n < 1 || m < 0) return SQB_E_DIMENSION;
-  if (n > kWideFusedMaxN || ld < m || ldq < m) return SQB_E_ARGUMENT;
+  if (n > kWideGramMaxN || ld < m || ldq < m) return SQB_E_ARGUMENT;
   const int nn = static_cast<int>(n);
   Small s;
   SQB_TRY(small_slots(ctx, nn, &s));
@@ -1266,7 +1285,7 @@ int sqb_cholqr2_sharded_dev(sqb_context* ctx, const double* d_x, int64_t m_local
                             int64_t ld, double* d_r) {
   SQB_TRY(enter(ctx));
   if (n < 1 || m_local < 0) return SQB_E_DIMENSION;
-  if (n > kWideFusedMaxN || ld < m_local) return SQB_E_ARGUMENT;
+  if (n > kWideGramMaxN || ld < m_local) return SQB_E_ARGUMENT;
   const int nn = static_cast<int>(n);
   if (nn > 64)
     return cholqr2_wide(ctx, plain_view(d_x, ld, nn), m_local, nn, d_r,

@@ -30,6 +30,8 @@ struct sqb_context {
   size_t ring_doubles = 0;
   cudaEvent_t ring_free[kRing] = {nullptr, nullptr, nullptr};
   long long host_slab_bytes = 256ll << 20;  // slab size of the host-pointer paths (sqb_set_host_slab_bytes)
+  double* qslab = nullptr;  // row slab of Q = X F for the 129..256-column fused sweeps
+  size_t qslab_doubles = 0;
   double* gen = nullptr;  // scratch of sqb_generate_dev
   size_t gen_doubles = 0;
 

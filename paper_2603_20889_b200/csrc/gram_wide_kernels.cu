@@ -309,6 +309,25 @@ __global__ void bfrag_wide_kernel(const double* __restrict__ b, int n, double* _
   }
 }
 
+// Block (row0.., col0..) of a dense column-major matrix `a` (leading dimension ld; rows x cols live
+// entries, zero beyond) into the fused kernel's fragment order; OP_SOLVE keeps the upper triangle of
+// the block only.  Used by the 128 < n <= 256 drivers, whose factor is cut into 128 x 128 blocks.
+template <int OP>
+__global__ void frag_from_dense_kernel(const double* __restrict__ a, long long ld, int row0, int col0, int rows,
+                                       int cols, double* __restrict__ frags) {
+  for (int idx = threadIdx.x + blockIdx.x * blockDim.x; idx < fused_frag_doubles(OP); idx += blockDim.x * gridDim.x) {
+    int row, col;
+    fused_frag_coord<OP>(idx, &row, &col);
+    const bool live = row < rows && col < cols && (OP == OP_MULTIPLY || row <= col);
+    frags[idx] = live ? a[(row0 + row) + static_cast<long long>(col0 + col) * ld] : 0.0;
+  }
+}
+
+// c += d (n x n): the row-slab partial sums of the 256-column drivers, added in ascending slab order
+__global__ void add_square_kernel(double* __restrict__ c, const double* __restrict__ d, int count) {
+  for (int idx = threadIdx.x + blockIdx.x * blockDim.x; idx < count; idx += blockDim.x * gridDim.x) c[idx] += d[idx];
+}
+
 // U = R^-1 by back substitution, thread j owns column j; written in the fused kernel's fragment order:
 // warp w, step f (f < 2w+2: tile column w, k-step f; else tile column 15-w, k-step f-2w-2),
 // lane (g,q): U[4k+q, 8j+g].  Also the reference's pre-check |R(j,j)| > n eps max|diag| (gram.cpp:126-134).
@@ -423,7 +442,8 @@ __device__ __forceinline__ void solve_panel(const double* stage, const double* r
 // lanes of a column 64 contiguous bytes
 template <int OP>
 __device__ __forceinline__ void solve_panel_out(const double* stage, const double* rf, double* qout, long long ldq,
-                                                long long r0, long long end, int n, int w, int lane, int g, int q) {
+                                                long long r0, long long end, int n, int n_out, int accumulate,
+                                                int w, int lane, int g, int q) {
   constexpr int NT = fused_rows(OP) / 8;
   const int j1 = w, j2 = kWT - 1 - w;
   double a1c[NT][2], a2c[NT][2];
@@ -434,8 +454,10 @@ __device__ __forceinline__ void solve_panel_out(const double* stage, const doubl
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       if (row + e < end) {
-        if (8 * j1 + g < n) qout[row + e + static_cast<long long>(8 * j1 + g) * ldq] = a1c[t][e];
-        if (8 * j2 + g < n) qout[row + e + static_cast<long long>(8 * j2 + g) * ldq] = a2c[t][e];
+        double* p1 = qout + row + e + static_cast<long long>(8 * j1 + g) * ldq;
+        double* p2 = qout + row + e + static_cast<long long>(8 * j2 + g) * ldq;
+        if (8 * j1 + g < n_out) *p1 = accumulate ? *p1 + a1c[t][e] : a1c[t][e];
+        if (8 * j2 + g < n_out) *p2 = accumulate ? *p2 + a2c[t][e] : a2c[t][e];
       }
     }
   }
@@ -449,6 +471,8 @@ struct WideSolveParams {
   double* partial;      // one 128 x 128 column-major slab per CTA
   double* qout;         // WRITEQ: Q = X U goes here (leading dimension ldq) and no Gram is formed
   long long ldq;
+  int n_out;            // WRITEQ: live output columns (<= 128); n counts the live X columns (the K extent)
+  int accumulate;       // WRITEQ: add to what qout holds (second K block of a 256-column product)
 };
 
 template <int OP, bool WRITEQ>
@@ -535,7 +559,9 @@ __global__ void __launch_bounds__(kWThreads, 1) gram_wide_fused_kernel(const Wid
         phase_bits ^= 1u << s;
       }
       const double* stage = smem + s * kStageDoubles;
-      if (WRITEQ) solve_panel_out<OP>(stage, rf, prm.qout, prm.ldq, begin + pn * P, end, prm.n, warp, lane, g, q);
+      if (WRITEQ)
+        solve_panel_out<OP>(stage, rf, prm.qout, prm.ldq, begin + pn * P, end, prm.n, prm.n_out, prm.accumulate, warp,
+                            lane, g, q);
       else solve_panel<OP>(stage, rf, qbuf + (pn & 1) * kQDoubles, prm.n, warp, lane, g, q);
     }
   }
@@ -647,6 +673,8 @@ static WideSolveParams fused_params(const MatView& x, long long m, int n, const 
   prm.partial = nullptr;
   prm.qout = nullptr;
   prm.ldq = 0;
+  prm.n_out = n;
+  prm.accumulate = 0;
   const long long panels = (m + fused_rows(op) - 1) / fused_rows(op);
   prm.kb = static_cast<int>(panels < sm_count ? (panels > 0 ? panels : 1) : sm_count);
   return prm;
@@ -684,6 +712,97 @@ cudaError_t launch_apply_rinv_wide(const double* x, long long m, int n, long lon
   prm.qout = q;
   prm.ldq = ldq;
   return launch_fused<OP_SOLVE, true>(prm, stream);
+}
+
+// ---- 128 < n <= 256: the Gram-based methods at BASELINE config 5's upper column count ---------------------
+// At 256 columns the sweep is 64 flop per byte of X - an order of magnitude past the machine balance - and
+// the factor (512 KB) no longer fits beside the stages, so Q = X F is formed explicitly, 128 output columns
+// and 128 contraction columns at a time, with the same fused GEMM kernel writing to a row-slab buffer, and
+// the wide SYRK runs on that slab.  The extra traffic (Q written once, read by the SYRK) is about a fifth
+// of the tensor-pipe time of the sweep; no m x n intermediate ever exists, only the slab.
+size_t gram_wide2_scratch_doubles(int n) {
+  return 2 * static_cast<size_t>(n) * n + 4 * static_cast<size_t>(fused_frag_doubles(OP_MULTIPLY));
+}
+
+// Q(rows [0, m), 256 columns) = X F for F = R^-1 (OP_SOLVE) or B (OP_MULTIPLY); frag sets f00, f01, f10, f11
+static cudaError_t wide2_apply(const MatView& x, long long m, int n, int op, const double* const f[4], int sm_count,
+                               double* q, long long ldq, cudaStream_t stream) {
+  const int n1 = n - kWC;
+  const MatView x0{x.base, x.ld, nullptr, kWC};
+  const MatView x1{x.base + static_cast<long long>(kWC) * x.ld, x.ld, nullptr, n1};
+  auto run = [&](const MatView& xv, int ncols, const double* frags, bool tri, double* qo, int n_out, int acc) {
+    WideSolveParams prm = fused_params(xv, m, ncols, frags, sm_count, tri ? OP_SOLVE : OP_MULTIPLY);
+    prm.qout = qo;
+    prm.ldq = ldq;
+    prm.n_out = n_out;
+    prm.accumulate = acc;
+    return tri ? launch_fused<OP_SOLVE, true>(prm, stream) : launch_fused<OP_MULTIPLY, true>(prm, stream);
+  };
+  const bool tri = op == OP_SOLVE;
+  cudaError_t e = run(x0, kWC, f[0], tri, q, kWC, 0);                                  // Q0  = X0 F00
+  if (e == cudaSuccess && !tri) e = run(x1, n1, f[2], false, q, kWC, 1);               // Q0 += X1 F10
+  if (e == cudaSuccess) e = run(x0, kWC, f[1], false, q + kWC * ldq, n1, 0);           // Q1  = X0 F01
+  if (e == cudaSuccess) e = run(x1, n1, f[3], tri, q + kWC * ldq, n1, 1);              // Q1 += X1 F11
+  return e;
+}
+
+// factor (n x n column-major: R or B) -> the four 128 x 128 fragment sets in `scratch`
+static cudaError_t wide2_factor(const double* factor, int n, int op, double* scratch, const double* f[4],
+                                StatusWord* status, cudaStream_t stream) {
+  const size_t nn = static_cast<size_t>(n) * n;
+  double* fr = scratch + 2 * nn;
+  const size_t fd = fused_frag_doubles(OP_MULTIPLY);
+  const int n1 = n - kWC;
+  const double* dense = factor;
+  if (op == OP_SOLVE) {
+    cudaError_t e = launch_rinv_global(factor, n, scratch, scratch + nn, status, stream);
+    if (e != cudaSuccess) return e;
+    dense = scratch + nn;
+    frag_from_dense_kernel<OP_SOLVE><<<64, 256, 0, stream>>>(dense, n, 0, 0, kWC, kWC, fr);
+    frag_from_dense_kernel<OP_SOLVE><<<64, 256, 0, stream>>>(dense, n, kWC, kWC, n1, n1, fr + 3 * fd);
+  } else {
+    frag_from_dense_kernel<OP_MULTIPLY><<<64, 256, 0, stream>>>(dense, n, 0, 0, kWC, kWC, fr);
+    frag_from_dense_kernel<OP_MULTIPLY><<<64, 256, 0, stream>>>(dense, n, kWC, 0, n1, kWC, fr + 2 * fd);
+    frag_from_dense_kernel<OP_MULTIPLY><<<64, 256, 0, stream>>>(dense, n, kWC, kWC, n1, n1, fr + 3 * fd);
+  }
+  frag_from_dense_kernel<OP_MULTIPLY><<<64, 256, 0, stream>>>(dense, n, 0, kWC, kWC, n1, fr + fd);
+  for (int i = 0; i < 4; ++i) f[i] = fr + i * fd;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gram_wide2_fused(const MatView& x, long long m, int n, int op, const double* factor, int sm_count,
+                                    double* scratch, double* qslab, long long slab_rows, double* partial,
+                                    double* c_tmp, double* c, StatusWord* status, cudaStream_t stream,
+                                    long long* launches) {
+  if (n <= kWC || n > kWideGramMaxN || (op != OP_SOLVE && op != OP_MULTIPLY) || slab_rows < 8) return cudaErrorInvalidValue;
+  const double* f[4];
+  cudaError_t e = wide2_factor(factor, n, op, scratch, f, status, stream);
+  if (e != cudaSuccess) return e;
+  *launches += 6;
+  e = cudaMemsetAsync(c, 0, sizeof(double) * n * n, stream);
+  for (long long r0 = 0; r0 < m && e == cudaSuccess; r0 += slab_rows) {
+    const long long rows = m - r0 < slab_rows ? m - r0 : slab_rows;
+    const MatView xs{x.base + r0, x.ld, nullptr, n};
+    e = wide2_apply(xs, rows, n, op, f, sm_count, qslab, slab_rows, stream);
+    if (e != cudaSuccess) break;
+    e = launch_gram_wide(MatView{qslab, slab_rows, nullptr, n}, rows, n, sm_count, partial, c_tmp, 0, status, stream);
+    if (e != cudaSuccess) break;
+    add_square_kernel<<<64, 256, 0, stream>>>(c, c_tmp, n * n);
+    e = cudaGetLastError();
+    *launches += (op == OP_SOLVE ? 3 : 4) + 3;
+  }
+  return e;
+}
+
+// Q = X R^-1 for 128 < n <= 256 (reference reconstruct_q, gram_qr.cpp:193-221), straight into q
+cudaError_t launch_apply_rinv_wide2(const double* x, long long m, int n, long long ld, const double* r, int sm_count,
+                                    double* scratch, double* q, long long ldq, StatusWord* status,
+                                    cudaStream_t stream) {
+  if (n <= kWC || n > kWideGramMaxN) return cudaErrorInvalidValue;
+  const double* f[4];
+  cudaError_t e = wide2_factor(r, n, OP_SOLVE, scratch, f, status, stream);
+  if (e != cudaSuccess) return e;
+  return wide2_apply(MatView{x, ld, nullptr, n}, m, n, OP_SOLVE, f, sm_count, q, ldq, stream);
 }
 
 }  // namespace sqb

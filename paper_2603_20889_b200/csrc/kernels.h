@@ -111,6 +111,18 @@ cudaError_t launch_apply_rinv_wide(const double* x, long long m, int n, long lon
                                    int sm_count, double* frags, double* q, long long ldq, StatusWord* status,
                                    cudaStream_t stream);
 
+// the same for 128 < n <= 256 (BASELINE config 5): Q = X F formed per row slab (128 x 128 factor blocks,
+// explicit R^-1), the wide SYRK on the slab.  scratch: gram_wide2_scratch_doubles(n); qslab: slab_rows x n
+// (leading dimension slab_rows, even); c_tmp: n x n
+size_t gram_wide2_scratch_doubles(int n);
+cudaError_t launch_gram_wide2_fused(const MatView& x, long long m, int n, int op, const double* factor, int sm_count,
+                                    double* scratch, double* qslab, long long slab_rows, double* partial,
+                                    double* c_tmp, double* c, StatusWord* status, cudaStream_t stream,
+                                    long long* launches);
+cudaError_t launch_apply_rinv_wide2(const double* x, long long m, int n, long long ld, const double* r, int sm_count,
+                                    double* scratch, double* q, long long ldq, StatusWord* status,
+                                    cudaStream_t stream);
+
 // ---- gram_thread_kernels.cu (n <= 8: register-resident rows and accumulators) --------------
 constexpr int kThreadGramMaxN = 8;
 cudaError_t launch_gram_thread(const GramParams& prm, int op, long long num_blocks,
@@ -121,8 +133,12 @@ int gram_thread_ctas_per_sm(int n, int op);
 
 // ---- small_kernels.cu (n x n work, one CTA each) -------------------------------------------
 constexpr int kSmallMaxN = 128;
+// n <= 128: one CTA, matrix in shared memory; beyond: in place in global memory (any n)
 cudaError_t launch_cholesky(const double* c, int n, double* r, StatusWord* status,
                             cudaStream_t stream);
+// U = R^-1 (n x n column-major) for any n; scratch_rowmajor: n x n doubles
+cudaError_t launch_rinv_global(const double* r, int n, double* scratch_rowmajor, double* u, StatusWord* status,
+                               cudaStream_t stream);
 cudaError_t launch_eigh(const double* c, int n, double* values, double* vectors, double* scratch,
                         StatusWord* status, cudaStream_t stream);
 // scratch: at least 4*n*n + 4*n doubles of device memory

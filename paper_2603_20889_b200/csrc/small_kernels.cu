@@ -85,6 +85,113 @@ __global__ void __launch_bounds__(kSmallThreads)
   }
 }
 
+// Cholesky beyond 128 columns (the reference's cholesky has no column limit, gram_qr.cpp:36-58; BASELINE
+// config 5 names n = 256): the matrix no longer fits one CTA's shared memory, so it is factored in place
+// in the output buffer (L2-resident, n = 256 is 512 KB) by one 1024-thread CTA, right-looking, row k staged
+// in shared memory for the rank-1 update.  Same per-entry operation order and breakdown rule as above.
+constexpr int kCholGlobalThreads = 1024;
+__global__ void __launch_bounds__(kCholGlobalThreads)
+    cholesky_global_kernel(const double* __restrict__ c, int n, double* __restrict__ r, StatusWord* status) {
+  extern __shared__ __align__(16) double rowk[];  // n doubles
+  __shared__ double tol_s, red_s[32];
+  __shared__ int fail_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double mx = 0.0;
+  for (int idx = tid; idx < n * n; idx += kCholGlobalThreads) {
+    const int i = idx % n, j = idx / n;
+    const double v = c[idx];
+    r[idx] = i <= j ? v : 0.0;
+    if (i == j) mx = fmax(mx, fabs(v));
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red_s[warp] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    double m2 = 0.0;
+    for (int w = 0; w < kCholGlobalThreads / 32; ++w) m2 = fmax(m2, red_s[w]);
+    tol_s = static_cast<double>(n) * kEps * m2;
+    fail_s = -1;
+  }
+  __syncthreads();
+  const double tol = tol_s;
+  const int tx = tid & 31, ty = tid >> 5;
+  for (int k = 0; k < n; ++k) {
+    const double d = r[k + static_cast<long long>(k) * n];
+    if (d <= tol) {
+      if (tid == 0) {
+        fail_s = k;
+        raise_status(status, SQB_E_BREAKDOWN, k);
+      }
+      break;
+    }
+    const double rkk = sqrt(d);
+    __syncthreads();  // everyone has read the pivot
+    for (int j = k + tid; j < n; j += kCholGlobalThreads) {
+      const double v = j == k ? rkk : r[k + static_cast<long long>(j) * n] / rkk;
+      r[k + static_cast<long long>(j) * n] = v;
+      rowk[j] = v;
+    }
+    __syncthreads();
+    for (int j = k + 1 + ty; j < n; j += 32) {
+      const double rkj = rowk[j];
+      double* col = r + static_cast<long long>(j) * n;
+      for (int i = k + 1 + tx; i <= j; i += 32) col[i] = fma(-rowk[i], rkj, col[i]);
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (fail_s >= 0)
+    for (int idx = tid; idx < n * n; idx += kCholGlobalThreads) r[idx] = 0.0;
+}
+
+// U = R^-1 for an upper triangular R of any order (the explicit inverse the wide fused sweeps multiply
+// with, see gram_wide_kernels.cu), one CTA, thread j owns column j: back substitution up the column.
+// `urm` is n x n scratch holding U row-major (the threads of a warp then touch consecutive addresses);
+// the result is written column-major to `u`.  Also the reference's pre-check
+// |R(j,j)| > n eps max|diag| (gram.cpp:126-134).
+__global__ void __launch_bounds__(256)
+    rinv_global_kernel(const double* __restrict__ r, int n, double* __restrict__ urm, double* __restrict__ u,
+                       StatusWord* status) {
+  __shared__ double red_s[8];
+  __shared__ double mx_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double mx = 0.0;
+  for (int j = tid; j < n; j += 256) mx = fmax(mx, fabs(r[j + static_cast<long long>(j) * n]));
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red_s[warp] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    double m2 = 0.0;
+    for (int w = 0; w < 8; ++w) m2 = fmax(m2, red_s[w]);
+    mx_s = m2;
+    const double dtol = static_cast<double>(n) * kEps * m2;
+    for (int j = 0; j < n; ++j)
+      if (fabs(r[j + static_cast<long long>(j) * n]) <= dtol) {
+        raise_status(status, SQB_E_SINGULAR, j);
+        break;
+      }
+  }
+  for (int j = tid; j < n; j += 256) {
+    for (int i = n - 1; i > j; --i) urm[static_cast<long long>(i) * n + j] = 0.0;
+    urm[static_cast<long long>(j) * n + j] = 1.0 / r[j + static_cast<long long>(j) * n];
+    for (int i = j - 1; i >= 0; --i) {
+      double s0 = 0.0, s1 = 0.0;
+      int k = i + 1;
+      for (; k + 1 <= j; k += 2) {
+        s0 = fma(r[i + static_cast<long long>(k) * n], urm[static_cast<long long>(k) * n + j], s0);
+        s1 = fma(r[i + static_cast<long long>(k + 1) * n], urm[static_cast<long long>(k + 1) * n + j], s1);
+      }
+      if (k <= j) s0 = fma(r[i + static_cast<long long>(k) * n], urm[static_cast<long long>(k) * n + j], s0);
+      urm[static_cast<long long>(i) * n + j] = -(s0 + s1) / r[i + static_cast<long long>(i) * n];
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < n * n; idx += 256) {
+    const int i = idx % n, j = idx / n;
+    u[idx] = urm[static_cast<long long>(i) * n + j];
+  }
+}
+
 // ------------------------------------------------------------------------------------------------
 // Symmetric eigensolver: Jacobi with the reference's rotation formulas, skip rule (a_pq == 0),
 // stopping test off(A) <= 10*n*eps*|C|_F checked once per sweep, 30-sweep cap and stable
@@ -413,7 +520,7 @@ __global__ void __launch_bounds__(kJacobiMaxThreads)
 // out = A B for upper-triangular A, B (small.cpp:9-20): sum over t in [i, j], ascending.
 __global__ void tri_multiply_kernel(const double* __restrict__ a, const double* __restrict__ b, int n,
                                     double* __restrict__ out) {
-  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+  for (int idx = threadIdx.x + blockIdx.x * blockDim.x; idx < n * n; idx += blockDim.x * gridDim.x) {
     const int i = idx % n, j = idx / n;
     double s = 0.0;
     if (i <= j)
@@ -425,7 +532,7 @@ __global__ void tri_multiply_kernel(const double* __restrict__ a, const double* 
 // out = A B, dense n x n (small.cpp:22-32)
 __global__ void small_multiply_kernel(const double* __restrict__ a, const double* __restrict__ b,
                                       int n, double* __restrict__ out) {
-  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+  for (int idx = threadIdx.x + blockIdx.x * blockDim.x; idx < n * n; idx += blockDim.x * gridDim.x) {
     const int i = idx % n, j = idx / n;
     double s = 0.0;
     for (int t = 0; t < n; ++t) s = fma(a[i + t * n], b[t + j * n], s);
@@ -571,10 +678,20 @@ cudaError_t opt_in_smem(K kernel, size_t bytes) {
 
 cudaError_t launch_cholesky(const double* c, int n, double* r, StatusWord* status,
                             cudaStream_t stream) {
+  if (n > kSmallMaxN) {
+    cholesky_global_kernel<<<1, kCholGlobalThreads, sizeof(double) * n, stream>>>(c, n, r, status);
+    return cudaGetLastError();
+  }
   const size_t bytes = sizeof(double) * static_cast<size_t>(n) * (n + 1);
   cudaError_t e = opt_in_smem(cholesky_kernel, bytes);
   if (e != cudaSuccess) return e;
   cholesky_kernel<<<1, kSmallThreads, bytes, stream>>>(c, n, r, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rinv_global(const double* r, int n, double* scratch_rowmajor, double* u, StatusWord* status,
+                               cudaStream_t stream) {
+  rinv_global_kernel<<<1, 256, 0, stream>>>(r, n, scratch_rowmajor, u, status);
   return cudaGetLastError();
 }
 
@@ -600,13 +717,13 @@ cudaError_t launch_svqb_pass(const double* c, int n, double* b, double* z, doubl
 
 cudaError_t launch_tri_multiply(const double* a, const double* b, int n, double* out,
                                 cudaStream_t stream) {
-  tri_multiply_kernel<<<1, 256, 0, stream>>>(a, b, n, out);
+  tri_multiply_kernel<<<n > 64 ? (n * n + 4095) / 4096 : 1, 256, 0, stream>>>(a, b, n, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_small_multiply(const double* a, const double* b, int n, double* out,
                                   cudaStream_t stream) {
-  small_multiply_kernel<<<1, 256, 0, stream>>>(a, b, n, out);
+  small_multiply_kernel<<<n > 64 ? (n * n + 4095) / 4096 : 1, 256, 0, stream>>>(a, b, n, out);
   return cudaGetLastError();
 }
 

@@ -147,22 +147,18 @@ def test_wide_gram(ctx, sq, oracle, m, n):
     cu = ctx.tsmttsm(big.t()[1:m + 1, :])
     ctx.synchronize()
     assert np.linalg.norm(cu.cpu().numpy() - c_ref) <= 5 * n * EPS * xn2
-    # the fused solve / multiply stop at 128 columns, tsmttsm at 256
-    if n > 128:
-        with pytest.raises(sq.ArgumentError):
-            ctx.tsmmttsmm(x, np.eye(n))
-        with pytest.raises(sq.ArgumentError):
-            ctx.tsmRttsmR(x, np.eye(n))
     x[m // 2, n - 1] = np.inf
     with pytest.raises(sq.ArgumentError):
         ctx.tsmttsm(x)
 
 
-@pytest.mark.parametrize("m,n", [(4000, 65), (5003, 100), (9000, 128), (20011, 127), (300, 128), (128, 128)])
+@pytest.mark.parametrize("m,n", [(4000, 65), (5003, 100), (9000, 128), (20011, 127), (300, 128), (128, 128),
+                                 (7001, 129), (6000, 200), (10007, 256), (300, 256), (40000, 256)])
 def test_wide_solve_gram_and_cholqr2(ctx, sq, oracle, m, n):
-    """64 < n <= 128: the reference's tsmRttsmR / cholqr2 have no column limit (gram.cpp:123-140,
-    gram_qr.cpp:123-131); fused solve + Gram DMMA kernel (explicit R^-1 GEMM feeding the SYRK) against
-    the oracle, host and device entry points, aligned and unaligned staging, error parity."""
+    """64 < n <= 256: the reference's tsmRttsmR / cholqr2 / cholesky have no column limit (gram.cpp:123-140,
+    gram_qr.cpp:36-58, 123-131; BASELINE config 5 names n = 128 / 256); fused solve + Gram DMMA kernel
+    (explicit R^-1 GEMM feeding the SYRK; beyond 128 columns per row slab through 128 x 128 factor blocks)
+    against the oracle, host and device entry points, aligned and unaligned staging, error parity."""
     import torch
     x = gaussian(m, n, seed=5 * n + m)
     c_ref = oracle.best.tsmttsm(x)
@@ -219,7 +215,8 @@ def test_wide_solve_gram_and_cholqr2(ctx, sq, oracle, m, n):
     assert np.array_equal(r_again, r)
 
 
-@pytest.mark.parametrize("m,n", [(4000, 65), (5003, 100), (9000, 128), (20011, 127), (300, 128)])
+@pytest.mark.parametrize("m,n", [(4000, 65), (5003, 100), (9000, 128), (20011, 127), (300, 128), (7001, 129),
+                                 (6000, 200), (10007, 256)])
 def test_wide_multiply_gram_and_svqb2(ctx, sq, oracle, m, n):
     """64 < n <= 128: tsmmttsmm (gram.cpp:142-151) and svqb2 (gram_qr.cpp:178-191; eigh_small's own
     limit is 128 columns, gram_qr.cpp:62) through the fused multiply + Gram DMMA kernel."""
@@ -245,6 +242,10 @@ def test_wide_multiply_gram_and_svqb2(ctx, sq, oracle, m, n):
     bad[n - 1, n - 2] = np.nan
     with pytest.raises(sq.ArgumentError):
         ctx.tsmmttsmm(x, bad)
+    if n > 128:  # eigh_small's own limit (gram_qr.cpp:62)
+        with pytest.raises(sq.ArgumentError):
+            ctx.svqb2(x)
+        return
     # SVQB2
     tr, z, sg, rank = ctx.svqb2(x)
     tr_ref, z_ref, sg_ref, rank_ref = oracle.best.svqb2(x)
@@ -264,19 +265,33 @@ def test_wide_gram_limit(ctx, sq):
     with pytest.raises(sq.ArgumentError):
         ctx.svqb2(gaussian(300, 129))
     with pytest.raises(sq.ArgumentError):
-        ctx.cholqr2(gaussian(300, 129))
+        ctx.cholqr2(gaussian(300, 257))
+    with pytest.raises(sq.ArgumentError):
+        ctx.tsmRttsmR(gaussian(300, 257), np.eye(257))
     with pytest.raises(sq.ArgumentError):
         ctx.tsmttsm(gaussian(300, 257))
 
 
-@pytest.mark.parametrize("n", [1, 2, 5, 8, 17, 32, 64])
-def test_cholesky_and_eigh(ctx, oracle, n):
+@pytest.mark.parametrize("n", [1, 2, 5, 8, 17, 32, 64, 128, 129, 200, 256])
+def test_cholesky_and_eigh(ctx, sq, oracle, n):
     a = gaussian(4 * n + 3, n, seed=n)
     c = np.asfortranarray(a.T @ a)
     r = ctx.cholesky(c)
     r_ref = oracle.best.cholesky(c)
     assert np.all(np.tril(r, -1) == 0.0)
     assert np.linalg.norm(r - r_ref) <= 50 * n * EPS * np.linalg.norm(r_ref) * np.linalg.cond(c) ** 0.5
+    if n > 1:  # breakdown parity: same pivot index as the reference (gram_qr.cpp:39-54)
+        cb = c.copy(order="F")
+        k = n // 2
+        cb[k, :] = cb[k - 1, :]
+        cb[:, k] = cb[:, k - 1]
+        with pytest.raises(sq.BreakdownError) as ei:
+            ctx.cholesky(cb)
+        with pytest.raises(oracle.OracleError) as eo:
+            oracle.best.cholesky(cb)
+        assert ei.value.pivot_index == eo.value.index == k
+    if n > 128:
+        return
     vals, vecs = ctx.eigh_small(c)
     vals_ref, _ = oracle.best.eigh_small(c)
     assert np.all(np.diff(vals) <= 0.0)

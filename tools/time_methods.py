@@ -1,5 +1,6 @@
 """Quick device-side timing of one method over a list of column counts.
-python tools/timeit.py METHOD n1,n2,... [LOG2_ELEMS] [REPS]   (m = 2^LOG2_ELEMS / n rows)"""
+python tools/time_methods.py METHOD n1,n2,... [LOG2_ELEMS] [REPS] [KERNEL]   (m = 2^LOG2_ELEMS / n rows;
+KERNEL = auto | thread | fold | mma forces a TSQR kernel family)"""
 import sys
 from pathlib import Path
 
@@ -13,6 +14,8 @@ log2e = int(sys.argv[3]) if len(sys.argv) > 3 else 29
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 5
 ctx = sq.Context(0)
 ctx.use_torch_stream()
+if len(sys.argv) > 5:
+    ctx.set_tsqr_kernel(sys.argv[5])
 for n in ns:
     m = (1 << log2e) // n
     m -= m % 2
