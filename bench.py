@@ -456,6 +456,11 @@ def run_headline(rig, args):
                                  "model_time_s": model_s, "model_ratio": ms * 1e-3 / model_s}
                     if meth == "tsqr":
                         row[meth]["fp64_tflops_2mn2"] = 2.0 * m * nn * nn / (ms * 1e-3) / 1e12
+                        # north_star "sustains": the same reps after 300 ms of back-to-back steps (power cap)
+                        ms_s, _ = rig.timed(lambda: run_method(xs, meth), args.sweep_reps, 3, spinup_ms=300.0)
+                        row[meth]["sustained_gbs"] = 8.0 * m * nn / (ms_s * 1e-3) / 1e9
+                        row[meth]["sustained_frac_8TBs"] = row[meth]["sustained_gbs"] / NOMINAL_HBM_GBS
+                        time.sleep(0.3)
                 except sq.Error as exc:
                     row[meth] = {"error": type(exc).__name__}
             sweep.append(row)

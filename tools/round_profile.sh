@@ -2,7 +2,7 @@
 # Everything the round's evidence needs, on one B200: bench (both arms), launch list, full ncu captures
 # of every streaming kernel family, clocks during the bench, BASELINE configs C1/C3/C4/C5.
 set -x
-TAG=${1:-r01}
+TAG=${1:-r02}
 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/${TAG}_gpu_tests.txt
 O=gpurun_out
 mkdir -p $O
@@ -11,6 +11,7 @@ SMI=$!
 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err
 kill $SMI
 python bench.py --impl reference --steps 5 --warmup 1 > $O/${TAG}_bench_reference.json 2>> $O/${TAG}_bench.err
+python bench.py --config c4 --steps 10 --warmup 3 > $O/${TAG}_bench_c4.json 2>> $O/${TAG}_bench.err
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-sweep > $O/${TAG}_bench_under_ncu.log 2>&1
 prof() { # name kernel-regex method n log2m : full capture, kept as the raw-metrics CSV (the .ncu-rep files
          # together exceed what gpurun brings back); the source page is kept for the headline kernels
@@ -48,7 +49,8 @@ prof3() { # the fused wide sweeps (64 < n <= 128): second streaming launch of ch
 }
 prof3 gram_wide_solve_n128 cholqr2
 prof3 gram_wide_multiply_n128 svqb2
+prof gram_wide2_gemm_n256 gram_wide_fused cholqr2 256 22
 python tools/time_gram_wide.py 24 > $O/${TAG}_wide.txt 2>&1
 python tools/run_configs.py $TAG > $O/${TAG}_configs.log 2>&1
-bash tools/sanitize.sh > /dev/null 2>&1
+bash tools/sanitize.sh $TAG > /dev/null 2>&1
 ls -la $O

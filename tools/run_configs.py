@@ -191,11 +191,13 @@ for n in (64, 128, 256):
     c_ref = ref.tsmttsm(xh)
     row["parity_err_F_at_2^17_rows"] = float(np.linalg.norm(c_gpu.cpu().numpy() - c_ref))
     row["parity_bound_5_n_eps_normX2"] = float(5 * n * EPS * np.linalg.norm(xh) ** 2)
-    if n <= 128:  # CholQR2 / SVQB2 through the fused wide sweeps (n <= 128), parity against the reference
+    if n <= 256:  # CholQR2 (n <= 256) / SVQB2 (n <= 128, eigh_small's limit), parity against the reference
         row["cholqr2_ms"] = gpu_ms(lambda: ctx.cholqr2(x), 3, 1)
         row["cholqr2_gbs_effective"] = 8.0 * m * n / row["cholqr2_ms"] / 1e6
-        row["svqb2_ms"] = gpu_ms(lambda: ctx.svqb2(x), 3, 1)
-        row["svqb2_gbs_effective"] = 8.0 * m * n / row["svqb2_ms"] / 1e6
+        row["cholqr2_second_sweep_useful_tflops_2mn2"] = 2.0 * m * n * n / (row["cholqr2_ms"] - ms) / 1e9
+        if n <= 128:
+            row["svqb2_ms"] = gpu_ms(lambda: ctx.svqb2(x), 3, 1)
+            row["svqb2_gbs_effective"] = 8.0 * m * n / row["svqb2_ms"] / 1e6
         r_gpu = ctx.cholqr2(x[:mc])
         ctx.synchronize()
         r_ref = ref.cholqr2(xh)
