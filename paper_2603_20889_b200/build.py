@@ -39,7 +39,7 @@ def _stale(target: Path, deps) -> bool:
 
 # (8-column tiles, 8-row groups per panel, warps per CTA) instances of the DMMA TSQR kernel, one
 # translation unit each (tsqr_mma_inst.cu) - keep in sync with SQB_MMA_CONFIGS in tsqr_mma_kernels.cu
-MMA_CONFIGS = [(2, 8, 8), (3, 8, 8), (4, 8, 8), (5, 6, 8), (6, 6, 8), (7, 6, 8), (8, 6, 8)]
+MMA_CONFIGS = [(2, 16, 8), (3, 12, 8), (4, 10, 8), (5, 8, 8), (6, 6, 8), (7, 6, 8), (8, 6, 8)]
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:

@@ -28,9 +28,15 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                : "d"(a), "d"(b));
 }
 
-template <int NB, int OP>
+// NB full 8-column tiles go through the tensor pipe; R in 1..4 REMAINDER columns (n = 8 NB + R) are
+// handled on the FMA pipe instead of paying for a whole padded tile column of DMMAs (at n = 33 that
+// padded tile column was half of the kernel's time): every lane dots its own fragments with the
+// remainder columns, which it reads from the stage as warp-wide broadcasts.
+template <int NB, int OP, int R = 0>
 struct GramCfg {
-  static constexpr int NPAD = 8 * NB;
+  static constexpr int NT = NB + (R > 0 ? 1 : 0);  // tile slots of the n x n side (factor, CTA sum)
+  static constexpr int NCOL = 8 * NB + R;          // staged columns
+  static constexpr int NPAD = 8 * NT;
   static constexpr int NW = 8;  // whole multiples of 4 warps: 6 would leave two SM sub-partitions half idle
   static constexpr int NS = 2;
   // OP_SOLVE: blocked substitution on the tensor cores (8 x 8 diagonal blocks by their explicit
@@ -64,28 +70,30 @@ struct GramCfg {
       kBlockedSolve ? kBlockedP[NB - 1]
                     : (OP == OP_SOLVE ? kSolveP[NB - 1] : (OP == OP_PLAIN ? kPlainP[NB - 1] : kMultP[NB - 1]));
   static constexpr int PP = stage_pitch(P, (OP == OP_MULTIPLY || kBlockedSolve) ? 4 : 8);
-  static constexpr int kStageDoubles = NPAD * PP;
+  static constexpr int kStageDoubles = NCOL * PP;
   static constexpr int kVbuf = 0;
   static constexpr int kWarpDoubles = NS * kStageDoubles + kVbuf;
   static constexpr int FP = NPAD + 4;  // factor pitch: conflict-free A-fragment reads
   static constexpr int kDinvPitch = 12;  // (4k+q) + 12 g: conflict-free A-fragment reads of an 8 x 8 block
   static constexpr int kFacDoubles =
-      OP == OP_PLAIN ? 0 : NPAD * FP + NPAD + (kBlockedSolve ? NB * 8 * kDinvPitch : 0);
+      OP == OP_PLAIN ? 0 : NPAD * FP + NPAD + (kBlockedSolve ? NT * 8 * kDinvPitch : 0);
   static constexpr int kSumDoubles = NPAD * NPAD;  // aliases the warp stages after the streaming loop
   static_assert(kSumDoubles <= kWarpDoubles * NW, "the CTA sum must fit into the stage area");
   static constexpr size_t kSmemBytes =
       sizeof(double) * (static_cast<size_t>(kWarpDoubles) * NW + kFacDoubles);
   static constexpr int NPAIR = NB * (NB + 1) / 2;
   static_assert(P >= 8 && P % 8 == 0, "panel rows");
-  static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
+  static_assert(kSmemBytes * kCtas + 1024 * kCtas <= 227 * 1024, "shared memory budget");
+  static_assert(R == 0 || (OP != OP_MULTIPLY && (OP == OP_PLAIN || kBlockedSolve)), "remainder variants");
 };
 
-template <int NB, int OP>
-__global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, GramCfg<NB, OP>::kCtas)
+template <int NB, int OP, int R>
+__global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP, R>::kCtas)
     gram_mma_kernel(const GramParams prm) {
-  using Cfg = GramCfg<NB, OP>;
+  using Cfg = GramCfg<NB, OP, R>;
   constexpr int P = Cfg::P, PP = Cfg::PP, NW = Cfg::NW, NS = Cfg::NS, NPAD = Cfg::NPAD;
-  constexpr int FP = Cfg::FP, NPAIR = Cfg::NPAIR;
+  constexpr int FP = Cfg::FP, NPAIR = Cfg::NPAIR, NT = Cfg::NT;
+  constexpr int RR = R > 0 ? R : 1;  // array extent of the remainder accumulators
   extern __shared__ __align__(128) double smem[];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -171,6 +179,13 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, GramCfg<NB, OP>::
   double acc[NPAIR][2];
 #pragma unroll
   for (int p = 0; p < NPAIR; ++p) acc[p][0] = acc[p][1] = 0.0;
+  // racc[b][k]: this lane's rows of (own column of tile b) . (remainder column k); b == NB is the
+  // remainder block against itself (lanes g < R)
+  double racc[NT][RR];
+#pragma unroll
+  for (int b = 0; b < NT; ++b)
+#pragma unroll
+    for (int k = 0; k < RR; ++k) racc[b][k] = 0.0;
   uint32_t phase_bits = 0;   // bit s = parity to wait for on stage s
   uint32_t async_bits = 0;   // bit s = stage s was filled by the async engine
 
@@ -216,6 +231,17 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, GramCfg<NB, OP>::
         for (int b = 0; b < NB; ++b)
 #pragma unroll
           for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], a[b].y, a[b2].y);
+        if constexpr (R > 0) {
+          double2 ar = make_double2(0.0, 0.0);
+          if (g < R) ar = *reinterpret_cast<const double2*>(stage + (8 * NB + g) * PP + 8 * t + 2 * q);
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            const double2 c = *reinterpret_cast<const double2*>(stage + (8 * NB + k) * PP + 8 * t + 2 * q);
+#pragma unroll
+            for (int b = 0; b < NB; ++b) racc[b][k] = fma(a[b].y, c.y, fma(a[b].x, c.x, racc[b][k]));
+            racc[NB][k] = fma(ar.y, c.y, fma(ar.x, c.x, racc[NB][k]));
+          }
+        }
       }
       __syncwarp();
       if (pnl + static_cast<long long>(NS) * NW < npanels) issue(pnl + static_cast<long long>(NS) * NW, s);
@@ -231,14 +257,17 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, GramCfg<NB, OP>::
       static_assert(!Cfg::kBlockedSolve || (P / 8) % TU == 0, "row groups per panel");
 #pragma unroll 1
       for (int t0 = 0; t0 < P / 8; t0 += TU) {
-        double2 y[TU][NB];
+        double2 y[TU][NT];
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {
+        for (int b = 0; b < NT; ++b) {
+          // the remainder block (b == NB, R live columns) keeps a tight stage: its dead lanes hold zeros
+          const bool live = b < NB || g < R;
           double* own = wstage + (8 * b + g) * PP + 8 * t0 + 2 * q;
           double z[TU][2];
 #pragma unroll
           for (int u = 0; u < TU; ++u) {
-            const double2 x2 = *reinterpret_cast<const double2*>(own + 8 * u);
+            double2 x2 = make_double2(0.0, 0.0);
+            if (live) x2 = *reinterpret_cast<const double2*>(own + 8 * u);
             z[u][0] = x2.x;
             z[u][1] = x2.y;
           }
@@ -252,8 +281,10 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, GramCfg<NB, OP>::
                 dmma884(z[u][0], z[u][1], af, wstage[(8 * a + 4 * kk + q) * PP + 8 * (t0 + u) + g]);
             }
           }
+          if (live) {
 #pragma unroll
-          for (int u = 0; u < TU; ++u) *reinterpret_cast<double2*>(own + 8 * u) = make_double2(z[u][0], z[u][1]);
+            for (int u = 0; u < TU; ++u) *reinterpret_cast<double2*>(own + 8 * u) = make_double2(z[u][0], z[u][1]);
+          }
           __syncwarp();
           double w[TU][2];
 #pragma unroll
@@ -261,14 +292,15 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, GramCfg<NB, OP>::
 #pragma unroll
           for (int kk = 0; kk < 2; ++kk) {
             const double af = dinv[b * 8 * Cfg::kDinvPitch + (4 * kk + q) + Cfg::kDinvPitch * g];
+            const bool zlive = b < NB || 4 * kk + q < R;
 #pragma unroll
             for (int u = 0; u < TU; ++u)
-              dmma884(w[u][0], w[u][1], af, wstage[(8 * b + 4 * kk + q) * PP + 8 * (t0 + u) + g]);
+              dmma884(w[u][0], w[u][1], af, zlive ? wstage[(8 * b + 4 * kk + q) * PP + 8 * (t0 + u) + g] : 0.0);
           }
           __syncwarp();  // every lane has read Z_b before Y_b replaces it
 #pragma unroll
           for (int u = 0; u < TU; ++u) {
-            *reinterpret_cast<double2*>(own + 8 * u) = make_double2(w[u][0], w[u][1]);
+            if (live) *reinterpret_cast<double2*>(own + 8 * u) = make_double2(w[u][0], w[u][1]);
             y[u][b] = make_double2(w[u][0], w[u][1]);
           }
           __syncwarp();
@@ -285,6 +317,14 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, GramCfg<NB, OP>::
           for (int b = 0; b < NB; ++b)
 #pragma unroll
             for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], y[u][b].y, y[u][b2].y);
+          if constexpr (R > 0) {
+#pragma unroll
+            for (int k = 0; k < R; ++k) {  // the finished remainder columns of Y, broadcast from the stage
+              const double2 c = *reinterpret_cast<const double2*>(wstage + (8 * NB + k) * PP + 8 * (t0 + u) + 2 * q);
+#pragma unroll
+              for (int b = 0; b < NT; ++b) racc[b][k] = fma(y[u][b].y, c.y, fma(y[u][b].x, c.x, racc[b][k]));
+            }
+          }
         }
       }
       __syncwarp();
@@ -405,6 +445,17 @@ __global__ void __launch_bounds__(GramCfg<NB, OP>::NW * kWarp, GramCfg<NB, OP>::
           csum[row + col * NPAD] += acc[p][0];
           csum[row + (col + 1) * NPAD] += acc[p][1];
         }
+      if constexpr (R > 0) {
+#pragma unroll
+        for (int b = 0; b < NT; ++b)
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            double sr = racc[b][k];
+            sr += __shfl_xor_sync(0xffffffffu, sr, 1);
+            sr += __shfl_xor_sync(0xffffffffu, sr, 2);
+            if (q == 0) csum[(8 * b + g) + (8 * NB + k) * NPAD] += sr;
+          }
+      }
     }
   }
   __syncthreads();
@@ -430,21 +481,45 @@ __global__ void gram_reduce_kernel(const double* partial, long long num_blocks, 
   }
 }
 
-template <int NB, int OP>
+template <int NB, int OP, int R = 0>
 static cudaError_t launch_gram_nb(const GramParams& prm, long long num_blocks, cudaStream_t stream) {
-  using Cfg = GramCfg<NB, OP>;
+  using Cfg = GramCfg<NB, OP, R>;
   static unsigned long long smem_ready = 0;  // per-device opt-in mask
   {
-    cudaError_t e = opt_in_dynamic_smem(gram_mma_kernel<NB, OP>, Cfg::kSmemBytes, &smem_ready);
+    cudaError_t e = opt_in_dynamic_smem(gram_mma_kernel<NB, OP, R>, Cfg::kSmemBytes, &smem_ready);
     if (e != cudaSuccess) return e;
   }
-  gram_mma_kernel<NB, OP>
+  gram_mma_kernel<NB, OP, R>
       <<<static_cast<unsigned>(num_blocks), Cfg::NW * kWarp, Cfg::kSmemBytes, stream>>>(prm);
   return cudaGetLastError();
 }
 
+// 8 NB + R columns with R in 1..4 and 2 <= NB <= 4 (17..20, 25..28, 33..36): remainder on the FMA pipe
+constexpr bool gram_remainder_variant(int n, int op) {
+  return op != OP_MULTIPLY && n % 8 >= 1 && n % 8 <= 4 && n / 8 >= 2 && n / 8 <= 4;
+}
+
+template <int NB, int OP>
+static cudaError_t launch_gram_rem(const GramParams& prm, long long num_blocks, cudaStream_t stream) {
+  switch (prm.n % 8) {
+    case 1: return launch_gram_nb<NB, OP, 1>(prm, num_blocks, stream);
+    case 2: return launch_gram_nb<NB, OP, 2>(prm, num_blocks, stream);
+    case 3: return launch_gram_nb<NB, OP, 3>(prm, num_blocks, stream);
+    default: return launch_gram_nb<NB, OP, 4>(prm, num_blocks, stream);
+  }
+}
+
 template <int OP>
 static cudaError_t launch_gram_op(const GramParams& prm, long long num_blocks, cudaStream_t stream) {
+  if constexpr (OP != OP_MULTIPLY) {
+    if (gram_remainder_variant(prm.n, OP)) {
+      switch (prm.n / 8) {
+        case 2: return launch_gram_rem<2, OP>(prm, num_blocks, stream);
+        case 3: return launch_gram_rem<3, OP>(prm, num_blocks, stream);
+        default: return launch_gram_rem<4, OP>(prm, num_blocks, stream);
+      }
+    }
+  }
   switch ((prm.n + 7) / 8) {
     case 1: return launch_gram_nb<1, OP>(prm, num_blocks, stream);
     case 2: return launch_gram_nb<2, OP>(prm, num_blocks, stream);
@@ -459,7 +534,7 @@ static cudaError_t launch_gram_op(const GramParams& prm, long long num_blocks, c
 }
 
 cudaError_t launch_gram(const GramParams& prm, int op, long long num_blocks, cudaStream_t stream) {
-  if (prm.n <= kThreadGramMaxN) return launch_gram_thread(prm, op, num_blocks, stream);
+  if (gram_use_thread(prm.n, op)) return launch_gram_thread(prm, op, num_blocks, stream);
   switch (op) {
     case OP_PLAIN: return launch_gram_op<OP_PLAIN>(prm, num_blocks, stream);
     case OP_SOLVE: return launch_gram_op<OP_SOLVE>(prm, num_blocks, stream);
@@ -476,8 +551,8 @@ cudaError_t launch_gram_reduce(const double* partial, long long num_blocks, int 
 }
 
 int gram_panel_rows(int n, int op) {
-  if (n <= kThreadGramMaxN) return gram_thread_chunk_rows(n, op);
-  const int nb = (n + 7) / 8;
+  if (gram_use_thread(n, op)) return gram_thread_chunk_rows(n, op);
+  const int nb = gram_remainder_variant(n, op) ? n / 8 : (n + 7) / 8;  // same tables, indexed by the full tiles
 #define SQB_CASE(NBV)                                                                   \
   case NBV:                                                                              \
     return op == OP_PLAIN ? GramCfg<NBV, OP_PLAIN>::P                                    \
@@ -491,13 +566,12 @@ int gram_panel_rows(int n, int op) {
 }
 
 int gram_warps(int n) {
-  if (n <= kThreadGramMaxN) return gram_thread_warps();
   return 8;
 }
 
 int gram_ctas_per_sm(int n, int op) {
-  if (n <= kThreadGramMaxN) return gram_thread_ctas_per_sm(n, op);
-  const int nb = (n + 7) / 8;
+  if (gram_use_thread(n, op)) return gram_thread_ctas_per_sm(n, op);
+  const int nb = gram_remainder_variant(n, op) ? n / 8 : (n + 7) / 8;
   if (SQB_GRAM_2CTA_NB2 && op != OP_PLAIN && nb == 2) return 2;
   return (SQB_GRAM_2CTA && (op == OP_PLAIN || SQB_GRAM_2CTA_ALL) && (nb == 3 || nb == 4)) ? 2 : 1;
 }

@@ -1,4 +1,4 @@
-// Thread-private fused Gram kernels for narrow matrices (n <= 8).
+// Thread-private fused Gram kernels for narrow matrices (n <= 12).
 //
 //   OP_PLAIN     C = X^T X                      reference tsmttsm    (src/gram.cpp:113-121)
 //   OP_SOLVE     C = (X R^-1)^T (X R^-1)        reference tsmRttsmR  (src/gram.cpp:123-140)
@@ -32,8 +32,9 @@ constexpr int kGT = 256;  // threads per CTA
 // accumulators + rows fit, which doubles the loads in flight.
 template <int N, int OP>
 struct GtCfg {
-  static constexpr int MINB = (OP == OP_MULTIPLY && N >= 5) ? 1 : 2;
-  static constexpr int P = (N >= 7 && OP != OP_MULTIPLY) ? 2 : 4;
+  // 9..12 columns: up to 78 accumulators + 2 rows of the panel per thread - one CTA per SM, 255 registers
+  static constexpr int MINB = ((OP == OP_MULTIPLY && N >= 5) || N >= 9) ? 1 : 2;
+  static constexpr int P = ((N >= 7 && OP != OP_MULTIPLY) || N >= 9) ? 2 : 4;
   static constexpr int kChunk = 32 * P;  // rows a warp consumes per step
 };
 
@@ -176,6 +177,10 @@ cudaError_t launch_op(const GramParams& prm, long long nb, cudaStream_t st) {
     case 6: gram_thread_kernel<6, OP><<<static_cast<unsigned>(nb), kGT, 0, st>>>(prm); break;
     case 7: gram_thread_kernel<7, OP><<<static_cast<unsigned>(nb), kGT, 0, st>>>(prm); break;
     case 8: gram_thread_kernel<8, OP><<<static_cast<unsigned>(nb), kGT, 0, st>>>(prm); break;
+    case 9: gram_thread_kernel<9, OP><<<static_cast<unsigned>(nb), kGT, 0, st>>>(prm); break;
+    case 10: gram_thread_kernel<10, OP><<<static_cast<unsigned>(nb), kGT, 0, st>>>(prm); break;
+    case 11: gram_thread_kernel<11, OP><<<static_cast<unsigned>(nb), kGT, 0, st>>>(prm); break;
+    case 12: gram_thread_kernel<12, OP><<<static_cast<unsigned>(nb), kGT, 0, st>>>(prm); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -194,9 +199,9 @@ cudaError_t launch_gram_thread(const GramParams& prm, int op, long long num_bloc
 }
 
 int gram_thread_chunk_rows(int n, int op) {
-  return (n >= 7 && op != OP_MULTIPLY) ? 64 : 128;  // GtCfg<N, OP>::kChunk
+  return ((n >= 7 && op != OP_MULTIPLY) || n >= 9) ? 64 : 128;  // GtCfg<N, OP>::kChunk
 }
 int gram_thread_warps() { return kGT / 32; }
-int gram_thread_ctas_per_sm(int n, int op) { return (op == OP_MULTIPLY && n >= 5) ? 1 : 2; }
+int gram_thread_ctas_per_sm(int n, int op) { return ((op == OP_MULTIPLY && n >= 5) || n >= 9) ? 1 : 2; }
 
 }  // namespace sqb

@@ -123,8 +123,11 @@ cudaError_t launch_apply_rinv_wide2(const double* x, long long m, int n, long lo
                                     double* scratch, double* q, long long ldq, StatusWord* status,
                                     cudaStream_t stream);
 
-// ---- gram_thread_kernels.cu (n <= 8: register-resident rows and accumulators) --------------
-constexpr int kThreadGramMaxN = 8;
+// ---- gram_thread_kernels.cu (n <= 12: register-resident rows and accumulators) -------------
+constexpr int kThreadGramMaxN = 12;
+// measured on B200 (profiles/README.md): the register-resident kernel wins the plain pass up to 10 columns,
+// the fused multiply pass up to 11 and the fused solve pass up to 12; beyond, the DMMA kernel
+inline bool gram_use_thread(int n, int op) { return n <= (op == OP_PLAIN ? 10 : (op == OP_MULTIPLY ? 11 : kThreadGramMaxN)); }
 cudaError_t launch_gram_thread(const GramParams& prm, int op, long long num_blocks,
                                cudaStream_t stream);
 int gram_thread_chunk_rows(int n, int op);

@@ -133,21 +133,20 @@ struct MmaFold {
                 make_double2(w[b][rr][0], w[b][rr][1]);
         }
         __syncwarp();
-        double vv[RG][2];
-#pragma unroll
-        for (int rr = 0; rr < RG; ++rr) {
-          const double2 t2 = *reinterpret_cast<const double2*>(stage + rr * PITCH + j * 10 + 2 * q);
-          vv[rr][0] = t2.x;
-          vv[rr][1] = t2.y;
-        }
+        // the broadcast column is re-read from the staging buffer wherever it is used (dot pass, update
+        // pass, trailing GEMMs) instead of being held: the registers go to a taller panel, and rows in
+        // flight per SM is what the latency-bound sweep's throughput is proportional to
+        const double* vsrc = stage + j * 10 + 2 * q;
         // one dot pass: v_j . (own column).  Own column == j: sigma.  Own column < j: Gram entry.
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
         for (int rp = 0; rp < RG / 2; ++rp) {
-          a0 = fma(vv[2 * rp][0], w[b][2 * rp][0], a0);
-          a1 = fma(vv[2 * rp][1], w[b][2 * rp][1], a1);
-          a2 = fma(vv[2 * rp + 1][0], w[b][2 * rp + 1][0], a2);
-          a3 = fma(vv[2 * rp + 1][1], w[b][2 * rp + 1][1], a3);
+          const double2 t2 = *reinterpret_cast<const double2*>(vsrc + (2 * rp) * PITCH);
+          const double2 u2 = *reinterpret_cast<const double2*>(vsrc + (2 * rp + 1) * PITCH);
+          a0 = fma(t2.x, w[b][2 * rp][0], a0);
+          a1 = fma(t2.y, w[b][2 * rp][1], a1);
+          a2 = fma(u2.x, w[b][2 * rp + 1][0], a2);
+          a3 = fma(u2.y, w[b][2 * rp + 1][1], a3);
         }
         const double dl = (a0 + a1) + (a2 + a3);
         // sigma straight from the four lanes of column j (independent shuffles: shorter than the
@@ -164,8 +163,9 @@ struct MmaFold {
         dcol[j] = g == j ? h.beta : fma(-h.u0, sv, rc);
 #pragma unroll
         for (int rr = 0; rr < RG; ++rr) {
-          w[b][rr][0] = fma(-vv[rr][0], sv, w[b][rr][0]);
-          w[b][rr][1] = fma(-vv[rr][1], sv, w[b][rr][1]);
+          const double2 t2 = *reinterpret_cast<const double2*>(vsrc + rr * PITCH);
+          w[b][rr][0] = fma(-t2.x, sv, w[b][rr][0]);
+          w[b][rr][1] = fma(-t2.y, sv, w[b][rr][1]);
         }
         u0p[0] = (2 * q == j) ? h.u0 : u0p[0];
         u0p[1] = (2 * q + 1 == j) ? h.u0 : u0p[1];
@@ -192,14 +192,10 @@ struct MmaFold {
             *reinterpret_cast<double2*>(tbuf + g * 8 + 2 * k) = make_double2(tn[2 * k], tn[2 * k + 1]);
         }
         __syncwarp();
-        double tb[2], vt[RG][2];
+        double tb[2];
         tb[0] = tbuf[(2 * q) * 8 + g];
         tb[1] = tbuf[(2 * q + 1) * 8 + g];
-#pragma unroll
-        for (int rr = 0; rr < RG; ++rr) {
-          vt[rr][0] = stage[rr * PITCH + (2 * q) * 10 + g];
-          vt[rr][1] = stage[rr * PITCH + (2 * q + 1) * 10 + g];
-        }
+        const double* vt0 = stage + (2 * q) * 10 + g;  // V^T fragments: row 8rr + g of reflector columns 2q, 2q+1
         // ---- trailing tiles: three small GEMMs on the tensor cores ------------------------------
         static_for<b + 1, NB>([&](auto tt) {
           constexpr int t = decltype(tt)::value;
@@ -220,8 +216,8 @@ struct MmaFold {
           *reinterpret_cast<double2*>(rt) = r2;
 #pragma unroll
           for (int rr = 0; rr < RG; ++rr) {
-            dmma(w[t][rr][0], w[t][rr][1], z0, vt[rr][0]);
-            dmma(w[t][rr][0], w[t][rr][1], z1, vt[rr][1]);
+            dmma(w[t][rr][0], w[t][rr][1], z0, vt0[rr * PITCH]);
+            dmma(w[t][rr][0], w[t][rr][1], z1, vt0[rr * PITCH + 10]);
           }
         });
       }

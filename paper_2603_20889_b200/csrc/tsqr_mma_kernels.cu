@@ -8,7 +8,7 @@ namespace sqb {
 
 // (8-column tiles, 8-row groups per panel, warps per CTA) - keep in sync with MMA_CONFIGS in build.py
 #define SQB_MMA_CONFIGS(X) \
-  X(2, 8, 8) X(3, 8, 8) X(4, 8, 8) X(5, 6, 8) X(6, 6, 8) X(7, 6, 8) X(8, 6, 8)
+  X(2, 16, 8) X(3, 12, 8) X(4, 10, 8) X(5, 8, 8) X(6, 6, 8) X(7, 6, 8) X(8, 6, 8)
 
 #define SQB_DECL(NBV, RGV, NWV) \
   cudaError_t launch_tsqr_mma_##NBV##_##RGV##_##NWV(const TsqrParams&, long long, cudaStream_t);
@@ -19,10 +19,10 @@ SQB_MMA_CONFIGS(SQB_DECL)
 // column count -> configuration (largest panel the register file holds: w takes 2*NB*RG doubles)
 #define SQB_MMA_SWITCH(EXPR)               \
   switch ((n + 7) / 8) {                   \
-    case 2: return EXPR(2, 8, 8);          \
-    case 3: return EXPR(3, 8, 8);          \
-    case 4: return EXPR(4, 8, 8);          \
-    case 5: return EXPR(5, 6, 8);          \
+    case 2: return EXPR(2, 16, 8);         \
+    case 3: return EXPR(3, 12, 8);         \
+    case 4: return EXPR(4, 10, 8);         \
+    case 5: return EXPR(5, 8, 8);          \
     case 6: return EXPR(6, 6, 8);          \
     case 7: return EXPR(7, 6, 8);          \
     default: return EXPR(8, 6, 8);         \

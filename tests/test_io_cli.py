@@ -118,13 +118,14 @@ def test_device_stream_and_cli_end_to_end(tmp_path, oracle):
     assert out.returncode == 0, out.stderr
     rows = json.loads(out.stdout)
     assert len(rows) == 12
-    # TSQR stops at 64 columns (tsqr.cpp:188), the Gram-based methods at 128 here
-    good = [r for r in rows if r["n"] <= 8 or (r["n"] == 65 and r["method"] != "tsqr")]
-    assert len(good) == 8
+    # TSQR stops at 64 columns (tsqr.cpp:188), SVQB2 at 128 (eigh_small, gram_qr.cpp:62), CholQR2 at 256 here
+    good = [r for r in rows if r["n"] <= 8 or (r["n"] == 65 and r["method"] != "tsqr")
+            or (r["n"] == 129 and r["method"] == "cholqr2")]
+    assert len(good) == 9
     assert all(isinstance(r["orth_resid"], float) and r["orth_resid"] <= 1e-12 and r["model_ratio"] > 0 for r in good)
     assert all(r["large_reads"] == (1 if r["method"] == "tsqr" else 2) * r["m"] * r["n"] for r in good)
     bad = [r for r in rows if r not in good]
-    assert len(bad) == 4 and all(r["orth_resid"] == "ArgumentError" for r in bad)  # per-row error, the grid continues
+    assert len(bad) == 3 and all(r["orth_resid"] == "ArgumentError" for r in bad)  # per-row error, the grid continues
     assert run_cli("bench", "--reps", "0").returncode != 0
 
 
