@@ -256,10 +256,16 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
       constexpr int TU = Cfg::kSolveUnroll;
       static_assert(!Cfg::kBlockedSolve || (P / 8) % TU == 0, "row groups per panel");
 #pragma unroll 1
+      // One remainder column is cheapest substituted on the FMA pipe (kRemFma); two to four go through the
+      // padded-tile DMMA substitution like a full block (the shuffle reductions of the FMA form cost more
+      // than the padded DMMAs from two columns on: measured, profiles/README.md) - their Gram products
+      // are formed on the FMA pipe either way.
+      constexpr bool kRemFma = R == 1;
+      constexpr int NSV = kRemFma ? NB : NT;  // tile slots the DMMA substitution walks
       for (int t0 = 0; t0 < P / 8; t0 += TU) {
         double2 y[TU][NT];
 #pragma unroll
-        for (int b = 0; b < NT; ++b) {
+        for (int b = 0; b < NSV; ++b) {
           // the remainder block (b == NB, R live columns) keeps a tight stage: its dead lanes hold zeros
           const bool live = b < NB || g < R;
           double* own = wstage + (8 * b + g) * PP + 8 * t0 + 2 * q;
@@ -305,6 +311,42 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
           }
           __syncwarp();
         }
+        // yr[u][k]: remainder column k of Y for this lane's two rows (the broadcast operand of the remainder
+        // Gram products)
+        double2 yr[TU][RR];
+        if constexpr (kRemFma) {
+          // y_c = (x_c - sum_{i < c} y_i R(i, c)) / R(c, c): a lane sums over its own columns of the full tiles
+          // (the strictly upper blocks of the factor are stored negated), three xor-shuffles over the column
+          // index g complete the sum; the result never goes back to the stage
+          constexpr int c = 8 * NB;
+          double fcol[NB];
+#pragma unroll
+          for (int b = 0; b < NB; ++b) fcol[b] = fac[(8 * b + g) + c * FP];
+          const double dinv_c = inv[c];
+#pragma unroll
+          for (int u = 0; u < TU; ++u) {
+            const double2 xr = *reinterpret_cast<const double2*>(wstage + c * PP + 8 * (t0 + u) + 2 * q);
+            double px = 0.0, py = 0.0;
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+              px = fma(fcol[b], y[u][b].x, px);
+              py = fma(fcol[b], y[u][b].y, py);
+            }
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+              px += __shfl_xor_sync(0xffffffffu, px, o);
+              py += __shfl_xor_sync(0xffffffffu, py, o);
+            }
+            yr[u][0] = make_double2((px + xr.x) * dinv_c, (py + xr.y) * dinv_c);
+            y[u][NB] = g == 0 ? yr[u][0] : make_double2(0.0, 0.0);
+          }
+        } else if constexpr (R > 0) {
+#pragma unroll
+          for (int u = 0; u < TU; ++u)
+#pragma unroll
+            for (int k = 0; k < R; ++k)
+              yr[u][k] = *reinterpret_cast<const double2*>(wstage + (8 * NB + k) * PP + 8 * (t0 + u) + 2 * q);
+        }
 #pragma unroll
         for (int u = 0; u < TU; ++u) {
           int p = 0;
@@ -319,8 +361,8 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
             for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], y[u][b].y, y[u][b2].y);
           if constexpr (R > 0) {
 #pragma unroll
-            for (int k = 0; k < R; ++k) {  // the finished remainder columns of Y, broadcast from the stage
-              const double2 c = *reinterpret_cast<const double2*>(wstage + (8 * NB + k) * PP + 8 * (t0 + u) + 2 * q);
+            for (int k = 0; k < R; ++k) {
+              const double2 c = yr[u][k];
 #pragma unroll
               for (int b = 0; b < NT; ++b) racc[b][k] = fma(y[u][b].y, c.y, fma(y[u][b].x, c.x, racc[b][k]));
             }
