@@ -28,16 +28,20 @@ prof tsqr_fold_n24 tsqr_fold stage1 24 26
 prof tsqr_mma_n32 tsqr_mma stage1 32 26
 prof tsqr_mma_n64 tsqr_mma stage1 64 25
 prof gram_thread_n8 gram_thread tsmttsm 8 27
+prof gram_thread_n10 gram_thread tsmttsm 10 27
 prof gram_mma_n16 gram_mma tsmttsm 16 27
+prof gram_mma_n33 gram_mma tsmttsm 33 26
 prof gram_mma_n32 gram_mma tsmttsm 32 26
 prof gram_mma_n64 gram_mma tsmttsm 64 25
 prof2() { # the SECOND matching launch of a cholqr2 call = the fused solve + Gram sweep (gram_*_kernel<.., OP_SOLVE>)
-  ncu --set full --clock-control none -k regex:$2 -s 1 -c 1 -o $O/${TAG}_$1 python tools/prof_run.py cholqr2 $3 $4 1 > /dev/null 2>&1
+  ncu --set full --clock-control none -k regex:$2 -s ${5:-1} -c 1 -o $O/${TAG}_$1 python tools/prof_run.py cholqr2 $3 $4 1 > /dev/null 2>&1
   ncu -i $O/${TAG}_$1.ncu-rep --page raw --csv > $O/${TAG}_$1.raw.csv 2>/dev/null
   rm -f $O/${TAG}_$1.ncu-rep
 }
 prof2 gram_solve_n8 gram_thread 8 27
+prof2 gram_solve_n12 gram_thread 12 27 0   # the plain pass at 12 columns is the DMMA kernel: first gram_thread launch
 prof2 gram_solve_n16 gram_mma 16 27
+prof2 gram_solve_n33 gram_mma 33 26
 prof2 gram_solve_n32 gram_mma 32 26
 prof2 gram_solve_n64 gram_mma 64 25
 prof gram_wide_n128 gram_wide_kernel tsmttsm 128 23
@@ -51,6 +55,8 @@ prof3 gram_wide_solve_n128 cholqr2
 prof3 gram_wide_multiply_n128 svqb2
 prof gram_wide2_gemm_n256 gram_wide_fused cholqr2 256 22
 python tools/time_gram_wide.py 24 > $O/${TAG}_wide.txt 2>&1
+ALLN=$(seq -s, 1 64)
+for meth in tsqr cholqr2 svqb2 tsmttsm; do python tools/time_methods.py $meth $ALLN 31 5 >> $O/${TAG}_all_n.txt 2>&1; done
 python tools/run_configs.py $TAG > $O/${TAG}_configs.log 2>&1
 bash tools/sanitize.sh $TAG > /dev/null 2>&1
 ls -la $O
