@@ -144,7 +144,7 @@ cudaError_t launch_rinv_global(const double* r, int n, double* scratch_rowmajor,
                                cudaStream_t stream);
 cudaError_t launch_eigh(const double* c, int n, double* values, double* vectors, double* scratch,
                         StatusWord* status, cudaStream_t stream);
-// scratch: at least 4*n*n + 4*n doubles of device memory
+// scratch: at least n*(n+1) + 2*n doubles of device memory (U beyond 64 columns, the two diagonal scalings)
 cudaError_t launch_svqb_pass(const double* c, int n, double* b, double* z, double* sigma,
                              long long* rank, int want_sigma, double* scratch, StatusWord* status,
                              cudaStream_t stream);

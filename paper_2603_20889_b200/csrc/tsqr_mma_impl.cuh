@@ -118,9 +118,7 @@ struct MmaFold {
         dcol[2 * k + 1] = t2.y;
       }
       double u0p[2] = {0.0, 0.0};
-      double tn[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) tn[j] = 0.0;
+      double gam[8];
 
       // ---- in-block sweep: 8 reflectors -------------------------------------------------------
       static_for<0, 8>([&](auto jj) {
@@ -169,13 +167,11 @@ struct MmaFold {
         }
         u0p[0] = (2 * q == j) ? h.u0 : u0p[0];
         u0p[1] = (2 * q + 1 == j) ? h.u0 : u0p[1];
-        // row g of -T: -T(g, j) = -gamma_j * sum_k (-T)(g, k) G(k, j), diagonal -gamma_j
-        double acc = 0.0;
-        static_for<0, j>([&](auto kk) {
-          constexpr int k = decltype(kk)::value;
-          acc = fma(tn[k], __shfl_sync(0xffffffffu, d, 4 * k), acc);
-        });
-        tn[j] = g == j ? -h.gamma : -h.gamma * acc;
+        // Gram entries of V for the T factor: G(k, j) = v_k . v_j is the finished dot d on lane group k < j;
+        // they go to the T buffer and -T is formed once per block after the sweep (in-order issue: a chain
+        // of j shuffle-fed FMAs inside the sweep stalled the warp ~170 clk per reflector)
+        gam[j] = h.gamma;
+        if (q == 0 && g < j) tbuf[g * 8 + j] = d;
       });
 
       // diagonal tile back to the triangle (all q hold the same column; q == 0 writes)
@@ -186,6 +182,21 @@ struct MmaFold {
       }
 
       if constexpr (b < NB - 1) {
+        // row g of -T from the Gram entries: -T(g, j) = -gamma_j * sum_{k<j} (-T)(g, k) G(k, j), diagonal
+        // -gamma_j (entries left of the diagonal come out as zero on their own); G read as broadcasts
+        __syncwarp();
+        double tn[8];
+        static_for<0, 8>([&](auto jj) {
+          constexpr int j = decltype(jj)::value;
+          double acc0 = 0.0, acc1 = 0.0;
+          static_for<0, j>([&](auto kk) {
+            constexpr int k = decltype(kk)::value;
+            if constexpr (k % 2 == 0) acc0 = fma(tn[k], tbuf[k * 8 + j], acc0);
+            else acc1 = fma(tn[k], tbuf[k * 8 + j], acc1);
+          });
+          tn[j] = g == j ? -gam[j] : -gam[j] * (acc0 + acc1);
+        });
+        __syncwarp();
         if (q == 0) {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
