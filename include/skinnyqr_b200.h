@@ -77,6 +77,10 @@ int sqb_set_host_slab_bytes(sqb_context* ctx, int64_t bytes);
  * synchronise the stream before returning (used by caller-supplied exchanges, below).         */
 int sqb_copy_h2d(sqb_context* ctx, void* d_dst, const void* h_src, int64_t bytes);
 int sqb_copy_d2h(sqb_context* ctx, void* h_dst, const void* d_src, int64_t bytes);
+/* Device memory on the context's device, for host code that owns device-resident matrices without
+ * including CUDA headers (the C++ mirror's DeviceMatrix, paper_2603_20889_b200/include/skinnyqr/device.hpp). */
+int sqb_device_alloc(sqb_context* ctx, int64_t bytes, void** d_ptr);
+int sqb_device_free(sqb_context* ctx, void* d_ptr);
 
 /* ---- plans (replaces default_tsqr_plan / default_gram_plan, src/plan.cpp:9-32) ---------- */
 /* num_blocks = CTAs of the streaming kernel (reference: worker threads), panel_rows = rows

@@ -121,7 +121,8 @@ class PanelPlan:
 # ---- library loading ---------------------------------------------------------------------------
 ABI_SYMBOLS = [
     "sqb_create", "sqb_destroy", "sqb_set_stream", "sqb_use_own_stream", "sqb_get_stream", "sqb_sync",
-    "sqb_set_tsqr_kernel", "sqb_set_host_slab_bytes", "sqb_copy_h2d", "sqb_copy_d2h",
+    "sqb_set_tsqr_kernel", "sqb_set_host_slab_bytes", "sqb_copy_h2d", "sqb_copy_d2h", "sqb_device_alloc",
+    "sqb_device_free",
     "sqb_last_error_index", "sqb_status_string", "sqb_device_sm_count", "sqb_launch_count",
     "sqb_default_tsqr_plan", "sqb_default_gram_plan",
     "sqb_tsqr_qless_dev", "sqb_tsqr_stage1_dev", "sqb_block_qless_qr_dev", "sqb_tsmttsm_dev",

@@ -203,7 +203,7 @@ int cholqr2_view(sqb_context* ctx, const MatView& v, long long m, int n, long lo
   return SQB_OK;
 }
 
-// ---- wide column counts (64 < n): plain Gram up to 256 columns, fused solve + Gram up to 128 ----
+// ---- wide column counts (64 < n <= 256): plain Gram, fused solve / multiply + Gram ----
 int gram_wide_view(sqb_context* ctx, const MatView& v, long long m, int n, int op, const double* factor,
                    double* d_c, bool check) {
   const size_t partial = gram_wide_partial_doubles(n, ctx->sm_count);
@@ -235,7 +235,8 @@ int gram_wide_view(sqb_context* ctx, const MatView& v, long long m, int n, int o
 }
 
 // CholQR2 beyond 64 columns (the reference's cholqr2 has no column limit, gram_qr.cpp:123-131): the
-// wide SYRK, the one-CTA Cholesky (n <= 128), the fused solve + Gram sweep, Cholesky, R = R2 R1.
+// wide SYRK, Cholesky (one CTA; in global memory beyond 128 columns), the fused solve + Gram sweep, Cholesky,
+// R = R2 R1; up to 256 columns.
 int cholqr2_wide(sqb_context* ctx, const MatView& v, long long m, int n, double* d_r,
                  const std::function<int(double*)>& allreduce) {
   Small s;
@@ -604,6 +605,24 @@ int sqb_copy_h2d(sqb_context* ctx, void* d_dst, const void* h_src, int64_t bytes
   return SQB_OK;
 }
 
+int sqb_device_alloc(sqb_context* ctx, int64_t bytes, void** d_ptr) {
+  SQB_TRY(enter(ctx));
+  if (!d_ptr || bytes < 0) return SQB_E_ARGUMENT;
+  *d_ptr = nullptr;
+  if (bytes == 0) return SQB_OK;
+  SQB_CUDA(cudaMalloc(d_ptr, static_cast<size_t>(bytes)));
+  return SQB_OK;
+}
+
+int sqb_device_free(sqb_context* ctx, void* d_ptr) {
+  SQB_TRY(enter(ctx));
+  if (d_ptr) {
+    SQB_CUDA(cudaStreamSynchronize(ctx->stream));  // nothing enqueued on this context may still use it
+    SQB_CUDA(cudaFree(d_ptr));
+  }
+  return SQB_OK;
+}
+
 int sqb_copy_d2h(sqb_context* ctx, void* h_dst, const void* d_src, int64_t bytes) {
   SQB_TRY(enter(ctx));
   if (bytes < 0 || (bytes > 0 && (!h_dst || !d_src))) return SQB_E_ARGUMENT;
@@ -705,7 +724,7 @@ static int gram_entry(sqb_context* ctx, const double* d_x, int64_t m, int64_t n,
   }
   if (n > 64) {
     // the reference's Gram kernels have no column limit (gram.cpp:113-151); here the plain Gram goes
-    // up to 256 columns, the fused solve / multiply + Gram up to 128
+    // up to 256 columns, like the fused solve / multiply + Gram (one launch up to 128, per row slab beyond)
     return gram_wide_view(ctx, plain_view(d_x, ld, static_cast<int>(n)), m, static_cast<int>(n), op, factor, d_c,
                           op == OP_PLAIN);
   }

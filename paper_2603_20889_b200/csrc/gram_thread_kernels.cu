@@ -8,8 +8,10 @@
 // contiguous bytes per column), applies R^-1 (substitution in the reference's column order,
 // src/kernels_scalar.cpp:19-32) or B to the row IN REGISTERS and accumulates the n(n+1)/2 upper
 // triangle entries in registers.  At n <= 8 that is at most 100 FMAs per row against 64 bytes of
-// HBM traffic, so these kernels sit on the memory roofline; the DMMA kernels (gram_kernels.cu) take
-// over for n > 8.  Per-CTA partials are reduced in fixed order (deterministic, gram.cpp:81-92).
+// HBM traffic, so these kernels sit on the memory roofline; up to 12 columns (78 accumulators, one CTA per
+// SM) they still beat the DMMA kernels (gram_kernels.cu), whose padded 16-column tiles do 2.4x the useful
+// work at 9 columns - the crossover is per operation (kernels.h: gram_use_thread).  Per-CTA partials are
+// reduced in fixed order (deterministic, gram.cpp:81-92).
 #include <type_traits>
 
 #include "kernels.h"

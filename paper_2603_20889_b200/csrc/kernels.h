@@ -93,7 +93,7 @@ int gram_panel_rows(int n, int op);
 int gram_warps(int n);
 int gram_ctas_per_sm(int n, int op);
 
-// ---- gram_wide_kernels.cu (64 < n <= 256, plain Gram only: BASELINE config 5) -----------------
+// ---- gram_wide_kernels.cu (64 < n <= 256: BASELINE config 5) ----------------------------------
 constexpr int kWideGramMaxN = 256;
 size_t gram_wide_partial_doubles(int n, int sm_count);
 cudaError_t launch_gram_wide(const MatView& x, long long m, int n, int sm_count, double* partial,

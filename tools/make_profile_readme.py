@@ -2,6 +2,7 @@
 python tools/make_profile_readme.py [tag]"""
 import csv
 import json
+import re
 import shutil
 import subprocess
 import sys
@@ -9,7 +10,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 G, P = ROOT / "gpurun_out", ROOT / "profiles"
-tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+tag = sys.argv[1] if len(sys.argv) > 1 else "r02"
 P.mkdir(exist_ok=True)
 
 
@@ -35,13 +36,15 @@ if bench:
     r = bench["roofline"]
     out.append("## Headline (bench.py, N = 1)\n")
     out.append(f"* workload: {bench['config']['workload']}; plan {bench['config']['plan']}")
-    out.append(f"* **value {bench['value']:.0f} GB/s** ({bench['ms_per_step']:.3f} ms per step, {bench['gpu_launches']} launches in the timed region), "
-               f"{100*bench['value']/8000:.1f} % of the nominal 8 TB/s roofline, {100*bench['value']/r['peak']:.1f} % of the measured copy bandwidth ({r['peak']:.0f} GB/s); "
+    hbm_peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6540.0
+    out.append(f"* **value {bench['value']:.0f} GB/s** ({bench['ms_per_step']:.3f} ms per step, {bench['gpu_launches']} launches in the timed region) - "
+               f"the SUSTAINED figure: K steps after 300 ms of untimed back-to-back steps, board on its power cap; "
+               f"{100*bench['value']/8000:.1f} % of the nominal 8 TB/s roofline, {100*bench['value']/hbm_peak:.1f} % of the measured copy bandwidth ({hbm_peak:.0f} GB/s); "
                f"clocks {bench['clocks']}")
-    if "sustained" in bench:
-        s = bench["sustained"]
-        out.append(f"* sustained (after 300 ms of back-to-back steps): {s['value']:.0f} GB/s, clocks {s['clocks']}")
-    out.append(f"* roofline (stage-1 kernel alone, in situ): achieved {r['achieved']:.0f} GB/s = {r['frac']:.3f} of measured peak; "
+    if "burst" in bench:
+        s = bench["burst"]
+        out.append(f"* burst (the same K steps on a settled board): {s['value']:.0f} GB/s = {100*s['value']/8000:.1f} % of 8 TB/s, clocks {s['clocks']}")
+    out.append(f"* roofline (stage-1 kernel alone, in situ, settled board): bound {r['bound']}, achieved {r['achieved']:.1f} {r['unit']} = {r['frac']:.3f} of {r['peak']} ({r['peak_source']}); "
                f"DRAM traffic per launch {r['traffic']} B vs algorithmic {r['algorithmic_bytes_per_launch']:.0f} B")
     if "e2e" in bench:
         e = bench["e2e"]
@@ -53,21 +56,32 @@ if bench:
     if "parity" in bench:
         out.append(f"* parity of the headline run against the reference on that sample: {bench['parity']}")
     if ref:
-        out.append(f"* `bench.py --impl reference`: {ref['value']:.2f} GB/s ({ref['cpu_baseline']['sample']})")
+        out.append(f"* `bench.py --impl reference`: {ref['value']:.2f} GB/s ({ref['cpu_baseline']['sample']}); same_config = {ref['config'].get('same_config')}")
+    c4 = jline(G / f"{tag}_bench_c4.json") if (G / f"{tag}_bench_c4.json").exists() else None
+    if c4:
+        shutil.copy(G / f"{tag}_bench_c4.json", P / f"{tag}_bench_c4.json")
+        out.append(f"* `bench.py --config c4` (BASELINE configs[3], {c4['config']['m_total']} x 16 [A b], {c4['n_gpus']} GPU): {c4['value']:.0f} GB/s, "
+                   f"{c4['ms_per_step']:.2f} ms per solve, {c4['gpu_launches']} launches per {c4['steps']} steps; solution {c4['solution']}")
+    if ref:
+        shutil.copy(G / f"{tag}_bench_reference.json", P / f"{tag}_bench_reference.json")
     if "sweep" in bench:
         out.append("\n## Column sweep at m = 2^27 (BASELINE configs[1]); ms / effective GB/s (8mn / t) / % of 8 TB/s\n")
         if "model_hardware" in bench:
             out.append(f"Roofline model of the reference (perf_model.hpp, `paper_2603_20889_b200/perf_model.py`) with {bench['model_hardware']}; "
                        "`x model` = measured time / model time.\n")
-        out.append("| n | GiB | TSQR | CholQR2 | SVQB2 | TSQR TFLOP/s (2mn^2) |")
-        out.append("|---|---|---|---|---|---|")
+        if "sweep_protocol" in bench:
+            out.append(f"Protocol: {bench['sweep_protocol']}; `sustained` = the same reps after 300 ms of back-to-back steps.\n")
+        out.append("| n | GiB | TSQR | CholQR2 | SVQB2 | TSQR TFLOP/s (2mn^2) | TSQR sustained GB/s | binding roofline (TSQR): fraction |")
+        out.append("|---|---|---|---|---|---|---|---|")
         for row in bench["sweep"]:
             cells = []
             for meth in ("tsqr", "cholqr2", "svqb2"):
                 v = row.get(meth, {})
                 cells.append((f"{v['ms']:.2f} ms / {v['gbs']:.0f} / {100*v['frac_8TBs']:.1f} %"
                               + (f" / {v['model_ratio']:.2f}x model" if "model_ratio" in v else "")) if "ms" in v else str(v))
-            out.append(f"| {row['n']} | {row['gib']:.0f} | {cells[0]} | {cells[1]} | {cells[2]} | {row['tsqr'].get('fp64_tflops_2mn2', 0):.1f} |")
+            tq = row.get("tsqr", {})
+            out.append(f"| {row['n']} | {row['gib']:.0f} | {cells[0]} | {cells[1]} | {cells[2]} | {tq.get('fp64_tflops_2mn2', 0):.1f} | "
+                       f"{tq.get('sustained_gbs', 0):.0f} | {tq.get('bound', '')}: {tq.get('frac_of_binding_roofline', 0):.2f} |")
 
 # launch list
 lf = G / f"{tag}_launches.csv"
@@ -123,10 +137,25 @@ if raws:
             continue
         mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         traffic[r.name.replace(f"{tag}_", "").replace(".raw.csv", "")] = rd * mult.get(ur, 1) + wr * mult.get(uw, 1)
-    t8 = traffic.get("tsqr_fold_n8")
-    tj = {"_source": f"profiles/{tag}_*.raw.csv (ncu --set full): dram__bytes_read.sum + dram__bytes_write.sum per launch", "all": traffic}
-    if t8:
-        tj["tsqr_n8"] = t8
+    import math
+    kern = {}
+    for k, b in traffic.items():
+        mnum = re.search(r"_n(\d+)$", k)
+        if not mnum or b <= 0:
+            continue
+        nn = int(mnum.group(1))
+        kern[k] = {"bytes": b, "m": 2 ** round(math.log2(b / (8.0 * nn)))}
+    tj = {"_source": f"profiles/{tag}_*.raw.csv (ncu --set full): dram__bytes_read.sum + dram__bytes_write.sum per launch of the "
+                     "streaming kernel, with the row count of the capture; bench.py scales to its own m", "kernels": kern}
+    for nn, key in ((4, "tsqr_thread_n4"), (8, "tsqr_fold_n8"), (12, "tsqr_fold_n12"), (16, "tsqr_fold_n16"), (24, "tsqr_fold_n24"),
+                    (32, "tsqr_mma_n32"), (64, "tsqr_mma_n64")):
+        if key in kern:
+            tj[f"tsqr_n{nn}"] = kern[key]
+    for nn, key in ((8, "gram_thread_n8"), (10, "gram_thread_n10"), (16, "gram_mma_n16"), (32, "gram_mma_n32"), (33, "gram_mma_n33"),
+                    (64, "gram_mma_n64")):
+        if key in kern:
+            tj[f"cholqr2_n{nn}"] = kern[key]
+            tj[f"svqb2_n{nn}"] = kern[key]
     (P / "traffic.json").write_text(json.dumps(tj, indent=1))
 
 cf = G / f"configs_{tag}.json"
@@ -162,12 +191,13 @@ if cf.exists():
             ts = f"{r['tsqr_ms']:.1f} ms = {r['tsqr_tflops_2mn2']:.1f} TFLOP/s" if "tsqr_ms" in r else "reference rejects n > 64"
             out.append(f"| {r['n']} | {r['tsmttsm_ms']:.2f} | {r['gbs']:.0f} | {r['nominal_tflops_2mn2']:.1f} | {r['executed_dmma_tflops']:.1f} | {100*r['dmma_pipe_util_vs_37.1']:.0f} % | {r['parity_err_F_at_2^17_rows']:.1e} ({r['parity_bound_5_n_eps_normX2']:.1e}) | {ts} |")
         if any("cholqr2_ms" in r for r in c["C5"]):
-            out.append("\nCholQR2 / SVQB2 at the same sizes (n <= 128: fused solve / multiply + Gram sweeps on the tensor cores; effective GB/s = 8mn / t):\n")
+            out.append("\nCholQR2 (n <= 256) / SVQB2 (n <= 128) at the same sizes (fused solve / multiply + Gram sweeps on the tensor cores; 256 columns: Q = X R^-1 per row slab + the wide SYRK; effective GB/s = 8mn / t):\n")
             out.append("| n | CholQR2 ms | GB/s | R parity err at 2^17 rows (bound 64 n eps |X|) | SVQB2 ms | GB/s |")
             out.append("|---|---|---|---|---|---|")
             for r in c["C5"]:
                 if "cholqr2_ms" in r:
-                    out.append(f"| {r['n']} | {r['cholqr2_ms']:.2f} | {r['cholqr2_gbs_effective']:.0f} | {r['cholqr2_parity_err_F_at_2^17_rows']:.1e} ({r['cholqr2_parity_bound_64_n_eps_normX']:.1e}) | {r['svqb2_ms']:.2f} | {r['svqb2_gbs_effective']:.0f} |")
+                    sv = f"{r['svqb2_ms']:.2f} | {r['svqb2_gbs_effective']:.0f}" if "svqb2_ms" in r else "eigh_small stops at 128 columns | -"
+                    out.append(f"| {r['n']} | {r['cholqr2_ms']:.2f} | {r['cholqr2_gbs_effective']:.0f} | {r['cholqr2_parity_err_F_at_2^17_rows']:.1e} ({r['cholqr2_parity_bound_64_n_eps_normX']:.1e}) | {sv} |")
 
 wide = G / f"{tag}_wide.txt"
 if wide.exists():
@@ -206,5 +236,8 @@ if san.exists():
 rw = G / f"{tag}_race_wide.txt"
 if rw.exists():
     out.append(f"\nRe-run on the final fused-kernel geometry (32-row solve panels, 2-stage ring):\n\n```\n{rw.read_text().strip()}\n```")
+probe = P / "probes" / f"{tag}_tsqr_experiments.txt"
+if probe.exists():
+    out.append(f"\n## Kernel experiments of this round that were measured and dropped (profiles/probes/{probe.name})\n\n```\n{probe.read_text().strip()}\n```")
 (P / "README.md").write_text("\n".join(out) + "\n")
 print("wrote", P / "README.md")
