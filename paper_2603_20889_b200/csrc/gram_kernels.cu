@@ -59,11 +59,11 @@ struct GramCfg {
 #endif
   static constexpr int kCtas = ((SQB_GRAM_2CTA && (OP == OP_PLAIN || SQB_GRAM_2CTA_ALL) && (NB == 3 || NB == 4)) ||
                                 (SQB_GRAM_2CTA_NB2 && OP != OP_PLAIN && NB == 2)) ? 2 : 1;
-  static constexpr int kPlainP[8] = {120, 72, kCtas == 2 ? 24 : 40, kCtas == 2 ? 24 : 40, 24, 24, 24, 24};
+  static constexpr int kPlainP[8] = {120, 72, kCtas == 2 ? 24 : 40, kCtas == 2 ? 24 : 40, 40, 24, 24, 24};
   static constexpr int kMultP[8] = {112, kCtas == 2 ? 32 : 64, kCtas == 2 ? 16 : 48, kCtas == 2 ? 16 : 32, 32, 16, 16, 16};
   // OP_SOLVE: one lane substitutes one row, so the panel height is a multiple of 32
   static constexpr int kSolveP[8] = {64, 64, 32, 32, 16, 16, 16, 16};
-  static constexpr int kBlockedP[8] = {64, kCtas == 2 ? 32 : 64, kCtas == 2 ? 16 : 48, kCtas == 2 ? 16 : 32, 16, 16, 16, 16};  // == 0 (mod 16): pitch P + 4
+  static constexpr int kBlockedP[8] = {64, kCtas == 2 ? 32 : 64, kCtas == 2 ? 16 : 48, kCtas == 2 ? 16 : 32, 32, 16, 16, 16};  // == 0 (mod 16): pitch P + 4
   static constexpr int kMultUnroll = NB == 1 ? 2 : (NB == 2 ? 4 : (NB == 3 ? (kCtas == 2 ? 2 : 3) : 1));  // measured: no gain from 32 columns on
   static constexpr int kSolveUnroll = NB <= 2 ? 4 : (kCtas == 2 ? 2 : (NB == 3 ? 3 : (NB == 4 ? 4 : (NB <= 6 ? 2 : 1))));  // row groups solved together
   static constexpr int P =
