@@ -261,8 +261,10 @@ __global__ void __launch_bounds__(kWThreads, 1) gram_wide_kernel(const WideParam
 // Panel geometry per variant.  The solve GEMM reads the X stage with the transposed LDS.64 pattern
 // ((4k+q) * pitch + 8t + g): conflict-free for pitch = 4 or 12 (mod 16); the SYRK reads the Q panel with
 // the LDS.128 pattern ((8T+g) * pitch + 8t + 2q): conflict-free for pitch = 8 (mod 16).
-__host__ __device__ constexpr int fused_rows(int op) { return op == OP_SOLVE ? 32 : 16; }
-__host__ __device__ constexpr int fused_spitch(int op) { return op == OP_SOLVE ? 36 : 20; }
+// `wq` (WRITEQ: Q goes to global memory, no shared Q panels and no SYRK accumulators) lets the dense
+// factor afford the 32-row panels too.
+__host__ __device__ constexpr int fused_rows(int op, bool wq = false) { return (op == OP_SOLVE || wq) ? 32 : 16; }
+__host__ __device__ constexpr int fused_spitch(int op, bool wq = false) { return (op == OP_SOLVE || wq) ? 36 : 20; }
 __host__ __device__ constexpr int fused_qpitch(int op) { return op == OP_SOLVE ? 40 : 24; }
 // k4 steps per warp: triangular factor (OP_SOLVE, U = R^-1) (2w+2) + (32-2w) = 34; dense factor
 // (OP_MULTIPLY, B) 32 + 32
@@ -274,8 +276,8 @@ __host__ __device__ constexpr int fused_frag_doubles(int op) { return 8 * fused_
 // two-stage ring is enough; the shared memory goes to taller panels (solve) / the dense factor's 128 KB
 // of fragments (multiply) instead
 __host__ __device__ constexpr int fused_stages(int) { return 2; }
-__host__ __device__ constexpr size_t fused_smem_doubles(int op) {
-  return static_cast<size_t>(fused_stages(op)) * kWC * fused_spitch(op) + 2 * kWC * fused_qpitch(op) +
+__host__ __device__ constexpr size_t fused_smem_doubles(int op, bool wq = false) {
+  return static_cast<size_t>(fused_stages(op)) * kWC * fused_spitch(op, wq) + (wq ? 0 : 2 * kWC * fused_qpitch(op)) +
          fused_frag_doubles(op);
 }
 constexpr double kEpsW = 2.220446049250313e-16;
@@ -388,11 +390,11 @@ __global__ void __launch_bounds__(128, 1)
 // Q[row 8t+2q+e, column 8J+g] in a?c[t][e].  One loop with run-time bounds for all warps (the warp index
 // only sets the trip counts), so the GEMM half of the kernel is not replicated eight times in the
 // instruction cache like the register-indexed SYRK has to be.
-template <int OP>
-__device__ __forceinline__ void solve_tiles(const double* stage, const double* rf, double (&a1c)[fused_rows(OP) / 8][2],
-                                            double (&a2c)[fused_rows(OP) / 8][2], int w, int kmax, int lane, int g,
+template <int OP, bool WQ = false>
+__device__ __forceinline__ void solve_tiles(const double* stage, const double* rf, double (&a1c)[fused_rows(OP, WQ) / 8][2],
+                                            double (&a2c)[fused_rows(OP, WQ) / 8][2], int w, int kmax, int lane, int g,
                                             int q) {
-  constexpr int NT = fused_rows(OP) / 8, SP = fused_spitch(OP);
+  constexpr int NT = fused_rows(OP, WQ) / 8, SP = fused_spitch(OP, WQ);
   // kmax = ceil(n / 4): columns of X beyond n are zero, so are the factor rows beyond n
   const int k1 = min(fused_k1(OP, w), kmax), k2 = min(fused_k2(OP, w), kmax);
 #pragma unroll
@@ -444,10 +446,10 @@ template <int OP>
 __device__ __forceinline__ void solve_panel_out(const double* stage, const double* rf, double* qout, long long ldq,
                                                 long long r0, long long end, int n, int n_out, int accumulate,
                                                 int w, int lane, int g, int q) {
-  constexpr int NT = fused_rows(OP) / 8;
+  constexpr int NT = fused_rows(OP, true) / 8;
   const int j1 = w, j2 = kWT - 1 - w;
   double a1c[NT][2], a2c[NT][2];
-  solve_tiles<OP>(stage, rf, a1c, a2c, w, (n + 3) / 4, lane, g, q);
+  solve_tiles<OP, true>(stage, rf, a1c, a2c, w, (n + 3) / 4, lane, g, q);
 #pragma unroll
   for (int t = 0; t < NT; ++t) {
     const long long row = r0 + 8 * t + 2 * q;
@@ -478,10 +480,10 @@ struct WideSolveParams {
 template <int OP, bool WRITEQ>
 __global__ void __launch_bounds__(kWThreads, 1) gram_wide_fused_kernel(const WideSolveParams prm) {
   extern __shared__ __align__(128) double smem[];
-  constexpr int NSTAGE = fused_stages(OP), P = fused_rows(OP), SP = fused_spitch(OP);
+  constexpr int NSTAGE = fused_stages(OP), P = fused_rows(OP, WRITEQ), SP = fused_spitch(OP, WRITEQ);
   __shared__ uint64_t bars[NSTAGE];
   constexpr int kQPitch = fused_qpitch(OP);
-  constexpr int kStageDoubles = kWC * SP, kQDoubles = kWC * kQPitch;
+  constexpr int kStageDoubles = kWC * SP, kQDoubles = WRITEQ ? 0 : kWC * kQPitch;
   double* qbuf = smem + NSTAGE * kStageDoubles;  // two Q panels
   double* rf = qbuf + 2 * kQDoubles;             // factor fragments
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -642,7 +644,7 @@ size_t gram_wide_fused_scratch_doubles() { return fused_frag_doubles(OP_MULTIPLY
 
 template <int OP, bool WRITEQ = false>
 static cudaError_t launch_fused(const WideSolveParams& prm, cudaStream_t stream) {
-  const size_t bytes = sizeof(double) * fused_smem_doubles(OP);
+  const size_t bytes = sizeof(double) * fused_smem_doubles(OP, WRITEQ);
   static unsigned long long smem_ready = 0;  // per-device opt-in mask
   {
     cudaError_t e = opt_in_dynamic_smem(gram_wide_fused_kernel<OP, WRITEQ>, bytes, &smem_ready);
@@ -664,7 +666,7 @@ static cudaError_t launch_rinv_wide(const double* r, int n, double* frags, Statu
 }
 
 static WideSolveParams fused_params(const MatView& x, long long m, int n, const double* frags, int sm_count,
-                                    int op) {
+                                    int op, bool wq = false) {
   WideSolveParams prm;
   prm.x = x;
   prm.m = m;
@@ -675,7 +677,7 @@ static WideSolveParams fused_params(const MatView& x, long long m, int n, const 
   prm.ldq = 0;
   prm.n_out = n;
   prm.accumulate = 0;
-  const long long panels = (m + fused_rows(op) - 1) / fused_rows(op);
+  const long long panels = (m + fused_rows(op, wq) - 1) / fused_rows(op, wq);
   prm.kb = static_cast<int>(panels < sm_count ? (panels > 0 ? panels : 1) : sm_count);
   return prm;
 }
@@ -708,7 +710,7 @@ cudaError_t launch_apply_rinv_wide(const double* x, long long m, int n, long lon
   if (n <= 64 || n > kWideFusedMaxN) return cudaErrorInvalidValue;
   cudaError_t e = launch_rinv_wide(r, n, frags, status, stream);
   if (e != cudaSuccess) return e;
-  WideSolveParams prm = fused_params(MatView{x, ld, nullptr, n}, m, n, frags, sm_count, OP_SOLVE);
+  WideSolveParams prm = fused_params(MatView{x, ld, nullptr, n}, m, n, frags, sm_count, OP_SOLVE, true);
   prm.qout = q;
   prm.ldq = ldq;
   return launch_fused<OP_SOLVE, true>(prm, stream);
@@ -731,7 +733,7 @@ static cudaError_t wide2_apply(const MatView& x, long long m, int n, int op, con
   const MatView x0{x.base, x.ld, nullptr, kWC};
   const MatView x1{x.base + static_cast<long long>(kWC) * x.ld, x.ld, nullptr, n1};
   auto run = [&](const MatView& xv, int ncols, const double* frags, bool tri, double* qo, int n_out, int acc) {
-    WideSolveParams prm = fused_params(xv, m, ncols, frags, sm_count, tri ? OP_SOLVE : OP_MULTIPLY);
+    WideSolveParams prm = fused_params(xv, m, ncols, frags, sm_count, tri ? OP_SOLVE : OP_MULTIPLY, true);
     prm.qout = qo;
     prm.ldq = ldq;
     prm.n_out = n_out;
