@@ -69,14 +69,29 @@ struct GramCfg {
   static constexpr int P =
       kBlockedSolve ? kBlockedP[NB - 1]
                     : (OP == OP_SOLVE ? kSolveP[NB - 1] : (OP == OP_PLAIN ? kPlainP[NB - 1] : kMultP[NB - 1]));
-  static constexpr int PP = stage_pitch(P, (OP == OP_MULTIPLY || kBlockedSolve) ? 4 : 8);
-  static constexpr int kStageDoubles = NCOL * PP;
+  // Blocked solve: the stage is read with the transposed LDS.64 pattern (DMMA B operands) AND read / written
+  // with the own-row 128-bit pattern.  A single pitch serves only one of them (pitch P + 4: 2-way conflicts on
+  // every 128-bit access, 3.2-3.8e8 per launch in ncu); pitch == 8 (mod 16) plus a 4-double offset of every
+  // second column pair serves both (kSwz), where the slightly larger stage still fits.
+  // At 64 columns the swizzled stage only fits when the factor is stored packed: the blocked solve reads
+  // nothing but the strictly upper 8 x 8 blocks (column 8b+g: rows 0..8b-1 at pitch 8b+4, which is
+  // 4 or 12 (mod 16): conflict-free A-fragment reads), the diagonal blocks live on as their inverses.
+  static constexpr bool kPackFac = kBlockedSolve && R == 0 && NB == 8;
+  static constexpr int kFacMain = kPackFac ? 32 * (NB * NB - 1) : NPAD * (NPAD + 4);
+  static constexpr int kFacDoublesPre = OP == OP_PLAIN ? 0 : kFacMain + NPAD + (kBlockedSolve ? NT * 8 * 12 : 0);
+  // measured: the swizzle pays where one CTA owns the SM (5..8 tiles: +8 % at 48 columns); the two-CTA
+  // configurations (16..32 columns) already run the tensor pipe at 83-87 % and gain nothing
+  static constexpr bool kSwz =
+      kBlockedSolve && kCtas == 1 &&
+      (sizeof(double) * (static_cast<size_t>(NS) * (NCOL * stage_pitch(P, 8) + 4) * NW + kFacDoublesPre) + 1024) <= 227 * 1024;
+  static constexpr int PP = kSwz ? stage_pitch(P, 8) : stage_pitch(P, (OP == OP_MULTIPLY || kBlockedSolve) ? 4 : 8);
+  static constexpr int kStageDoubles = NCOL * PP + (kSwz ? 4 : 0);
   static constexpr int kVbuf = 0;
   static constexpr int kWarpDoubles = NS * kStageDoubles + kVbuf;
   static constexpr int FP = NPAD + 4;  // factor pitch: conflict-free A-fragment reads
   static constexpr int kDinvPitch = 12;  // (4k+q) + 12 g: conflict-free A-fragment reads of an 8 x 8 block
-  static constexpr int kFacDoubles =
-      OP == OP_PLAIN ? 0 : NPAD * FP + NPAD + (kBlockedSolve ? NT * 8 * kDinvPitch : 0);
+  static constexpr int kFacDoubles = kFacDoublesPre;
+  static_assert(FP == NPAD + 4 && kDinvPitch == 12, "kFacDoublesPre assumes these pitches");
   static constexpr int kSumDoubles = NPAD * NPAD;  // aliases the warp stages after the streaming loop
   static_assert(kSumDoubles <= kWarpDoubles * NW, "the CTA sum must fit into the stage area");
   static constexpr size_t kSmemBytes =
@@ -93,6 +108,8 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
   using Cfg = GramCfg<NB, OP, R>;
   constexpr int P = Cfg::P, PP = Cfg::PP, NW = Cfg::NW, NS = Cfg::NS, NPAD = Cfg::NPAD;
   constexpr int FP = Cfg::FP, NPAIR = Cfg::NPAIR, NT = Cfg::NT;
+  constexpr bool SWZ = Cfg::kSwz;
+  auto coff = [](int c) { return stage_col_offset<PP, SWZ>(c); };  // stage offset of column c
   constexpr int RR = R > 0 ? R : 1;  // array extent of the remainder accumulators
   extern __shared__ __align__(128) double smem[];
 
@@ -108,8 +125,11 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
   __shared__ uint64_t bars_all[NW * NS];
   uint64_t* bars = bars_all + warp * NS;
   (void)vbuf;
-  double* fac = smem + static_cast<size_t>(NW) * Cfg::kWarpDoubles;  // NPAD x FP, then inv diag
-  double* inv = fac + NPAD * FP;
+  double* fac = smem + static_cast<size_t>(NW) * Cfg::kWarpDoubles;  // NPAD x FP (or packed), then inv diag
+  double* inv = fac + Cfg::kFacMain;
+  constexpr bool PACK = Cfg::kPackFac;
+  // element (row, column 8b+g) of the factor as the blocked solve reads it (row < 8b when packed)
+  auto fidx = [](int row, int b, int g) { return PACK ? 32 * (b * b - 1) + g * (8 * b + 4) + row : row + (8 * b + g) * FP; };
   double* csum = smem;  // reused once every warp has left the streaming loop
 
   for (int i = lane; i < NS * Cfg::kStageDoubles + Cfg::kVbuf; i += kWarp) my[i] = 0.0;
@@ -118,9 +138,11 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
   if (OP != OP_PLAIN) {
     for (int i = threadIdx.x; i < Cfg::kFacDoubles; i += NW * kWarp) fac[i] = 0.0;
     __syncthreads();
+    // packed factor: the full copy only exists during this prologue, in the (still idle) stage area
+    double* ff = PACK ? smem : fac;
     for (int i = threadIdx.x; i < n * n; i += NW * kWarp) {
       const int r = i % n, c = i / n;
-      if (OP == OP_MULTIPLY || r <= c) fac[r + c * FP] = prm.factor[i];
+      if (OP == OP_MULTIPLY || r <= c) ff[r + c * FP] = prm.factor[i];
     }
     __syncthreads();
     if constexpr (Cfg::kBlockedSolve) {
@@ -136,8 +158,8 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
           double v = i == j ? 1.0 : 0.0;
 #pragma unroll
           for (int k2 = i + 1; k2 < 8; ++k2)
-            if (k2 <= j) v = fma(-fac[(8 * b + i) + (8 * b + k2) * FP], xcol[k2], v);
-          const double dgn = (8 * b + i) < n ? fac[(8 * b + i) + (8 * b + i) * FP] : 1.0;
+            if (k2 <= j) v = fma(-ff[(8 * b + i) + (8 * b + k2) * FP], xcol[k2], v);
+          const double dgn = (8 * b + i) < n ? ff[(8 * b + i) + (8 * b + i) * FP] : 1.0;
           xcol[i] = i <= j ? v / dgn : 0.0;
         }
 #pragma unroll
@@ -149,11 +171,11 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
       // SingularFactorError(j) for the first offending j; inv_diag precomputed.
       if (threadIdx.x == 0) {
         double mx = 0.0;
-        for (int j = 0; j < n; ++j) mx = fmax(mx, fabs(fac[j + j * FP]));
+        for (int j = 0; j < n; ++j) mx = fmax(mx, fabs(ff[j + j * FP]));
         const double dtol = static_cast<double>(n) * 2.220446049250313e-16 * mx;
         int bad = -1;
         for (int j = 0; j < n; ++j) {
-          const double d = fac[j + j * FP];
+          const double d = ff[j + j * FP];
           if (bad < 0 && !(fabs(d) > dtol)) bad = j;
           inv[j] = 1.0 / d;
         }
@@ -164,7 +186,11 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
       __syncthreads();
       for (int i = threadIdx.x; i < NPAD * NPAD; i += NW * kWarp) {
         const int r = i % NPAD, c = i / NPAD;
-        if ((r >> 3) < (c >> 3)) fac[r + c * FP] = -fac[r + c * FP];
+        if ((r >> 3) < (c >> 3)) fac[fidx(r, c >> 3, c & 7)] = -ff[r + c * FP];
+      }
+      if constexpr (PACK) {  // give the stage area back as zeros
+        __syncthreads();
+        for (int i = threadIdx.x; i < NPAD * FP; i += NW * kWarp) smem[i] = 0.0;
       }
     }
   }
@@ -190,7 +216,7 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
   uint32_t async_bits = 0;   // bit s = stage s was filled by the async engine
 
   auto issue = [&](long long pnl, int s) {
-    const bool a = issue_panel<P, PP>(prm.x, n, begin + pnl * P, end, aligned,
+    const bool a = issue_panel<P, PP, SWZ>(prm.x, n, begin + pnl * P, end, aligned,
                                       my + s * Cfg::kStageDoubles, bars + s, lane);
     async_bits = a ? (async_bits | (1u << s)) : (async_bits & ~(1u << s));
   };
@@ -268,7 +294,7 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
         for (int b = 0; b < NSV; ++b) {
           // the remainder block (b == NB, R live columns) keeps a tight stage: its dead lanes hold zeros
           const bool live = b < NB || g < R;
-          double* own = wstage + (8 * b + g) * PP + 8 * t0 + 2 * q;
+          double* own = wstage + coff(8 * b + g) + 8 * t0 + 2 * q;
           double z[TU][2];
 #pragma unroll
           for (int u = 0; u < TU; ++u) {
@@ -281,10 +307,10 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
           for (int a = 0; a < b; ++a) {
 #pragma unroll
             for (int kk = 0; kk < 2; ++kk) {
-              const double af = fac[(8 * a + 4 * kk + q) + (8 * b + g) * FP];  // -R_ab
+              const double af = fac[fidx(8 * a + 4 * kk + q, b, g)];  // -R_ab
 #pragma unroll
               for (int u = 0; u < TU; ++u)
-                dmma884(z[u][0], z[u][1], af, wstage[(8 * a + 4 * kk + q) * PP + 8 * (t0 + u) + g]);
+                dmma884(z[u][0], z[u][1], af, wstage[coff(8 * a + 4 * kk + q) + 8 * (t0 + u) + g]);
             }
           }
           if (live) {
@@ -301,7 +327,7 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
             const bool zlive = b < NB || 4 * kk + q < R;
 #pragma unroll
             for (int u = 0; u < TU; ++u)
-              dmma884(w[u][0], w[u][1], af, zlive ? wstage[(8 * b + 4 * kk + q) * PP + 8 * (t0 + u) + g] : 0.0);
+              dmma884(w[u][0], w[u][1], af, zlive ? wstage[coff(8 * b + 4 * kk + q) + 8 * (t0 + u) + g] : 0.0);
           }
           __syncwarp();  // every lane has read Z_b before Y_b replaces it
 #pragma unroll
@@ -325,7 +351,7 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
           const double dinv_c = inv[c];
 #pragma unroll
           for (int u = 0; u < TU; ++u) {
-            const double2 xr = *reinterpret_cast<const double2*>(wstage + c * PP + 8 * (t0 + u) + 2 * q);
+            const double2 xr = *reinterpret_cast<const double2*>(wstage + coff(c) + 8 * (t0 + u) + 2 * q);
             double px = 0.0, py = 0.0;
 #pragma unroll
             for (int b = 0; b < NB; ++b) {
@@ -345,7 +371,7 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
           for (int u = 0; u < TU; ++u)
 #pragma unroll
             for (int k = 0; k < R; ++k)
-              yr[u][k] = *reinterpret_cast<const double2*>(wstage + (8 * NB + k) * PP + 8 * (t0 + u) + 2 * q);
+              yr[u][k] = *reinterpret_cast<const double2*>(wstage + coff(8 * NB + k) + 8 * (t0 + u) + 2 * q);
         }
 #pragma unroll
         for (int u = 0; u < TU; ++u) {

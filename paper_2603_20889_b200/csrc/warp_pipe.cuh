@@ -38,7 +38,14 @@ __device__ __forceinline__ bool view_bulk_aligned(const MatView& x, int n, long 
 // Fill one stage with rows [r0, min(r0+P, end)) of the n live columns.  Full, 16-byte aligned
 // panels go through the async engine (returns true: wait on `bar`); ragged or unaligned panels
 // are filled synchronously by the warp with zero padding (returns false).
-template <int P, int PP>
+// SWZ: column j starts 4 doubles later when bit 1 of j is set (stage_col_offset) - with a pitch == 8
+// (mod 16) that makes BOTH fragment patterns above conflict-free in one stage.
+template <int PP, bool SWZ>
+__host__ __device__ __forceinline__ constexpr int stage_col_offset(int j) {
+  return j * PP + (SWZ ? ((j & 2) << 1) : 0);
+}
+
+template <int P, int PP, bool SWZ = false>
 __device__ __forceinline__ bool issue_panel(const MatView& x, int n, long long r0, long long end,
                                             bool aligned, double* stage, uint64_t* bar, int lane) {
   const long long left = end - r0;
@@ -49,14 +56,14 @@ __device__ __forceinline__ bool issue_panel(const MatView& x, int n, long long r
     __syncwarp();
     for (int j = lane; j < n; j += kWarp) {
       fence_async_smem();
-      bulk_g2s(stage + j * PP, x.col(j) + r0, P * sizeof(double), bar);
+      bulk_g2s(stage + stage_col_offset<PP, SWZ>(j), x.col(j) + r0, P * sizeof(double), bar);
     }
     return true;
   }
   const int live = static_cast<int>(left < P ? left : P);
   for (int j = 0; j < n; ++j) {
     const double* src = x.col(j) + r0;
-    for (int r = lane; r < P; r += kWarp) stage[j * PP + r] = r < live ? __ldg(src + r) : 0.0;
+    for (int r = lane; r < P; r += kWarp) stage[stage_col_offset<PP, SWZ>(j) + r] = r < live ? __ldg(src + r) : 0.0;
   }
   __syncwarp();
   return false;
