@@ -123,6 +123,12 @@ struct MmaFold {
       // ---- in-block sweep: 8 reflectors -------------------------------------------------------
       static_for<0, 8>([&](auto jj) {
         constexpr int j = decltype(jj)::value;
+        // The last tile may hold fewer than 8 live columns (n = 8 (NB - 1) + r): its padding columns are
+        // exact zeros, their reflectors the identity, so their steps are skipped - at n = 33 the padded
+        // steps were a fifth of the kernel's reflector chains.  nx.n is the column count, warp-uniform.
+        if constexpr (b == NB - 1 && j > 0) {
+          if (8 * b + j >= nx.n) return;
+        }
         // broadcast column j of the panel (the dense part of reflector j) through the staging buffer
         if (g == j) {
 #pragma unroll
