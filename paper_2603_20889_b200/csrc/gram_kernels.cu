@@ -99,7 +99,7 @@ struct GramCfg {
   static constexpr int NPAIR = NB * (NB + 1) / 2;
   static_assert(P >= 8 && P % 8 == 0, "panel rows");
   static_assert(kSmemBytes * kCtas + 1024 * kCtas <= 227 * 1024, "shared memory budget");
-  static_assert(R == 0 || (OP != OP_MULTIPLY && (OP == OP_PLAIN || kBlockedSolve)), "remainder variants");
+  static_assert(R == 0 || OP == OP_PLAIN || OP == OP_MULTIPLY || kBlockedSolve, "remainder variants");
 };
 
 template <int NB, int OP, int R>
@@ -456,24 +456,26 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
       if (pnl + static_cast<long long>(NS) * NW < npanels) issue(pnl + static_cast<long long>(NS) * NW, s);
     } else {  // OP_MULTIPLY
       const int kchunks = (n + 3) / 4;
-      // MU row groups advance together: NB * MU independent DMMA chains of length kchunks, and every
+      // MU row groups advance together: NT * MU independent DMMA chains of length kchunks, and every
       // factor fragment is loaded once per MU groups
       constexpr int MU = Cfg::kMultUnroll;
       static_assert(OP != OP_MULTIPLY || (P / 8) % MU == 0, "row groups per panel");
 #pragma unroll 1
       for (int t0 = 0; t0 < P / 8; t0 += MU) {
-        double y[MU][NB][2];
+        double y[MU][NT][2];
 #pragma unroll
         for (int u = 0; u < MU; ++u)
 #pragma unroll
-          for (int b = 0; b < NB; ++b) y[u][b][0] = y[u][b][1] = 0.0;
+          for (int b = 0; b < NT; ++b) y[u][b][0] = y[u][b][1] = 0.0;
 #pragma unroll 1
         for (int kc = 0; kc < kchunks; ++kc) {
           double bf[MU];
+          // the stage holds exactly the n live columns when there is a remainder tile
+          const bool klive = R == 0 || 4 * kc + q < Cfg::NCOL;
 #pragma unroll
-          for (int u = 0; u < MU; ++u) bf[u] = stage[(4 * kc + q) * PP + 8 * (t0 + u) + g];
+          for (int u = 0; u < MU; ++u) bf[u] = klive ? stage[(4 * kc + q) * PP + 8 * (t0 + u) + g] : 0.0;
 #pragma unroll
-          for (int b = 0; b < NB; ++b) {
+          for (int b = 0; b < NT; ++b) {
             const double af = fac[(4 * kc + q) + (8 * b + g) * FP];
 #pragma unroll
             for (int u = 0; u < MU; ++u) dmma884(y[u][b][0], y[u][b][1], af, bf[u]);
@@ -491,6 +493,17 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
           for (int b = 0; b < NB; ++b)
 #pragma unroll
             for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], y[u][b][1], y[u][b2][1]);
+          if constexpr (R > 0) {
+            // remainder columns of X B sit in the accumulators of lane group k: one shuffle per row
+            // hands them to every column group, the products go to the FMA pipe
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+              const double c0 = __shfl_sync(0xffffffffu, y[u][NB][0], 4 * k + q);
+              const double c1 = __shfl_sync(0xffffffffu, y[u][NB][1], 4 * k + q);
+#pragma unroll
+              for (int b = 0; b < NT; ++b) racc[b][k] = fma(y[u][b][1], c1, fma(y[u][b][0], c0, racc[b][k]));
+            }
+          }
         }
       }
       __syncwarp();
@@ -563,8 +576,10 @@ static cudaError_t launch_gram_nb(const GramParams& prm, long long num_blocks, c
 }
 
 // 8 NB + R columns with R in 1..4 and 2 <= NB <= 4 (17..20, 25..28, 33..36): remainder on the FMA pipe
+// (the multiply pass only up to two remainder columns: its remainder entries reach the other column groups
+// through shuffles, which stop paying at three - measured)
 constexpr bool gram_remainder_variant(int n, int op) {
-  return op != OP_MULTIPLY && n % 8 >= 1 && n % 8 <= 4 && n / 8 >= 2 && n / 8 <= 4;
+  return n % 8 >= 1 && n % 8 <= (op == OP_MULTIPLY ? 2 : 4) && n / 8 >= 2 && n / 8 <= 4;
 }
 
 template <int NB, int OP>
@@ -579,13 +594,11 @@ static cudaError_t launch_gram_rem(const GramParams& prm, long long num_blocks, 
 
 template <int OP>
 static cudaError_t launch_gram_op(const GramParams& prm, long long num_blocks, cudaStream_t stream) {
-  if constexpr (OP != OP_MULTIPLY) {
-    if (gram_remainder_variant(prm.n, OP)) {
-      switch (prm.n / 8) {
-        case 2: return launch_gram_rem<2, OP>(prm, num_blocks, stream);
-        case 3: return launch_gram_rem<3, OP>(prm, num_blocks, stream);
-        default: return launch_gram_rem<4, OP>(prm, num_blocks, stream);
-      }
+  if (gram_remainder_variant(prm.n, OP)) {
+    switch (prm.n / 8) {
+      case 2: return launch_gram_rem<2, OP>(prm, num_blocks, stream);
+      case 3: return launch_gram_rem<3, OP>(prm, num_blocks, stream);
+      default: return launch_gram_rem<4, OP>(prm, num_blocks, stream);
     }
   }
   switch ((prm.n + 7) / 8) {
