@@ -12,10 +12,11 @@
 // update runs on the FP64 tensor pipe: lane (g,q) of a warp holds X[row(q), 8b+g], which is at
 // the same time the A fragment (8 columns x 4 rows, transposed) and the B fragment (4 rows x 8
 // columns) of mma.m8n8k4.f64 - so  C[8b.., 8b'..] += mma(w[b], w[b'])  needs no data movement.
-//   * OP_SOLVE: every lane takes one row of the staged panel into registers, applies R^-1 by
-//     column-oriented substitution (the order of the reference's trsm_right_upper,
-//     src/kernels_scalar.cpp:19-32) and puts the row back into the stage; the Gram MMAs then read
-//     the transformed panel - X R^-1 never leaves the SM.
+//   * OP_SOLVE substitutes by 8-column blocks on the tensor cores: Y_b^T = Rbb^-T (X_b^T - sum_{a<b} R_ab^T
+//     Y_a^T) with explicit inverses of the 8 x 8 diagonal blocks; finished blocks go back to the stage,
+//     where later blocks read them as B fragments - X R^-1 never leaves the SM.  (Up to 12 columns the
+//     register-resident kernel of gram_thread_kernels.cu substitutes column by column in the reference's
+//     order, src/kernels_scalar.cpp:19-32, and is faster.)
 //   * OP_MULTIPLY forms (X B) for 8 rows at a time with DMMAs whose accumulator layout is exactly
 //     the Gram fragment layout, then feeds those accumulators straight into the Gram MMAs.
 #include "kernels.h"
@@ -41,10 +42,8 @@ struct GramCfg {
   static constexpr int NS = 2;
   // OP_SOLVE: blocked substitution on the tensor cores (8 x 8 diagonal blocks by their explicit
   // inverses, everything off the diagonal as DMMA updates) instead of lane = row
-#ifndef SQB_BLOCKED_FROM
-#define SQB_BLOCKED_FROM 2  // measured: 4-9 % faster than lane = row substitution already at 16..32 columns
-#endif
-  static constexpr bool kBlockedSolve = OP == OP_SOLVE && NB >= SQB_BLOCKED_FROM;
+  static_assert(NB >= 2, "up to 8 columns every operation runs the register-resident kernel");
+  static constexpr bool kBlockedSolve = OP == OP_SOLVE;
   // streaming panel heights: P == 8 (mod 16) keeps the plain fragment pattern unpadded, P == 0
   // (mod 16) costs the transposed pattern only 4 pad rows
 #ifndef SQB_GRAM_2CTA
@@ -61,14 +60,11 @@ struct GramCfg {
                                 (SQB_GRAM_2CTA_NB2 && OP != OP_PLAIN && NB == 2)) ? 2 : 1;
   static constexpr int kPlainP[8] = {120, 72, kCtas == 2 ? 24 : 40, kCtas == 2 ? 24 : 40, 40, 24, 24, 24};
   static constexpr int kMultP[8] = {112, kCtas == 2 ? 32 : 64, kCtas == 2 ? 16 : 48, kCtas == 2 ? 16 : 32, 32, 16, 16, 16};
-  // OP_SOLVE: one lane substitutes one row, so the panel height is a multiple of 32
-  static constexpr int kSolveP[8] = {64, 64, 32, 32, 16, 16, 16, 16};
   static constexpr int kBlockedP[8] = {64, kCtas == 2 ? 32 : 64, kCtas == 2 ? 16 : 48, kCtas == 2 ? 16 : 32, 32, 16, 16, 16};  // == 0 (mod 16): pitch P + 4
   static constexpr int kMultUnroll = NB == 1 ? 2 : (NB == 2 ? 4 : (NB == 3 ? (kCtas == 2 ? 2 : 3) : 1));  // measured: no gain from 32 columns on
   static constexpr int kSolveUnroll = NB <= 2 ? 4 : (kCtas == 2 ? 2 : (NB == 3 ? 3 : (NB == 4 ? 4 : (NB <= 6 ? 2 : 1))));  // row groups solved together
   static constexpr int P =
-      kBlockedSolve ? kBlockedP[NB - 1]
-                    : (OP == OP_SOLVE ? kSolveP[NB - 1] : (OP == OP_PLAIN ? kPlainP[NB - 1] : kMultP[NB - 1]));
+      kBlockedSolve ? kBlockedP[NB - 1] : (OP == OP_PLAIN ? kPlainP[NB - 1] : kMultP[NB - 1]);
   // Blocked solve: the stage is read with the transposed LDS.64 pattern (DMMA B operands) AND read / written
   // with the own-row 128-bit pattern.  A single pitch serves only one of them (pitch P + 4: 2-way conflicts on
   // every 128-bit access, 3.2-3.8e8 per launch in ncu); pitch == 8 (mod 16) plus a 4-double offset of every
@@ -397,63 +393,6 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
       }
       __syncwarp();
       if (pnl + static_cast<long long>(NS) * NW < npanels) issue(pnl + static_cast<long long>(NS) * NW, s);
-    } else if (OP == OP_SOLVE) {
-      // W <- W R^-1 in place in the stage: lane = row, the whole row in registers, column-order
-      // substitution (kernels_scalar.cpp:19-32: subtract earlier columns ascending, then scale
-      // by the reciprocal diagonal); R is read as shared-memory broadcasts.
-      double* wstage = my + s * Cfg::kStageDoubles;
-#pragma unroll 1
-      for (int r0 = 0; r0 < P; r0 += kWarp) {
-        double* rowp = wstage + r0 + lane;
-        double y[NPAD];
-#pragma unroll
-        for (int j = 0; j < NPAD; ++j) y[j] = rowp[j * PP];
-        // right-looking form of the same recurrence: once y_i is final, every later column takes
-        // its -r_ij*y_i term (independent FMAs); per column the terms still arrive for ascending i
-        if constexpr (NB <= 4) {
-#pragma unroll
-          for (int i = 0; i < NPAD; ++i) {
-            y[i] *= inv[i];
-            rowp[i * PP] = y[i];
-#pragma unroll
-            for (int j = i + 1; j < NPAD; ++j) y[j] = fma(-fac[i + j * FP], y[i], y[j]);
-          }
-        } else {  // wide rows: left-looking keeps the register pressure read-only (the right-looking
-                  // form is demoted to local memory by nvcc beyond 32 columns)
-#pragma unroll
-          for (int j = 0; j < NPAD; ++j) {
-            double acc0 = y[j], acc1 = 0.0;
-#pragma unroll
-            for (int i = 0; i + 1 < j; i += 2) {
-              acc0 = fma(-fac[i + j * FP], y[i], acc0);
-              acc1 = fma(-fac[i + 1 + j * FP], y[i + 1], acc1);
-            }
-            if (j & 1) acc0 = fma(-fac[(j - 1) + j * FP], y[j - 1], acc0);
-            y[j] = (acc0 + acc1) * inv[j];
-            rowp[j * PP] = y[j];
-          }
-        }
-      }
-      __syncwarp();
-#pragma unroll 2
-      for (int t = 0; t < P / 8; ++t) {
-        double2 a[NB];
-#pragma unroll
-        for (int b = 0; b < NB; ++b)
-          a[b] = *reinterpret_cast<const double2*>(wstage + (8 * b + g) * PP + 8 * t + 2 * q);
-        int p = 0;
-#pragma unroll
-        for (int b = 0; b < NB; ++b)
-#pragma unroll
-          for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], a[b].x, a[b2].x);
-        p = 0;
-#pragma unroll
-        for (int b = 0; b < NB; ++b)
-#pragma unroll
-          for (int b2 = b; b2 < NB; ++b2, ++p) dmma884(acc[p][0], acc[p][1], a[b].y, a[b2].y);
-      }
-      __syncwarp();
-      if (pnl + static_cast<long long>(NS) * NW < npanels) issue(pnl + static_cast<long long>(NS) * NW, s);
     } else {  // OP_MULTIPLY
       const int kchunks = (n + 3) / 4;
       // MU row groups advance together: NT * MU independent DMMA chains of length kchunks, and every
@@ -602,7 +541,6 @@ static cudaError_t launch_gram_op(const GramParams& prm, long long num_blocks, c
     }
   }
   switch ((prm.n + 7) / 8) {
-    case 1: return launch_gram_nb<1, OP>(prm, num_blocks, stream);
     case 2: return launch_gram_nb<2, OP>(prm, num_blocks, stream);
     case 3: return launch_gram_nb<3, OP>(prm, num_blocks, stream);
     case 4: return launch_gram_nb<4, OP>(prm, num_blocks, stream);
@@ -639,7 +577,7 @@ int gram_panel_rows(int n, int op) {
     return op == OP_PLAIN ? GramCfg<NBV, OP_PLAIN>::P                                    \
                           : (op == OP_SOLVE ? GramCfg<NBV, OP_SOLVE>::P : GramCfg<NBV, OP_MULTIPLY>::P);
   switch (nb) {
-    SQB_CASE(1) SQB_CASE(2) SQB_CASE(3) SQB_CASE(4) SQB_CASE(5) SQB_CASE(6) SQB_CASE(7)
+    SQB_CASE(2) SQB_CASE(3) SQB_CASE(4) SQB_CASE(5) SQB_CASE(6) SQB_CASE(7)
     default: return op == OP_PLAIN ? GramCfg<8, OP_PLAIN>::P
                                    : (op == OP_SOLVE ? GramCfg<8, OP_SOLVE>::P : GramCfg<8, OP_MULTIPLY>::P);
   }

@@ -247,7 +247,10 @@ __device__ double block_sum(double v, double* red) {
   return out;
 }
 
-__device__ bool jacobi_eigh(double* a, int lda, double* u, int ldu, int n, const JacobiScratch& js) {
+// want_vectors = false skips every access to U (the sigma eigensolve of an SVQB pass only needs the eigenvalues;
+// beyond 64 columns U lives in global memory and is the larger half of a round's traffic).
+__device__ bool jacobi_eigh(double* a, int lda, double* u, int ldu, int n, const JacobiScratch& js,
+                            bool want_vectors = true) {
   const int tid = threadIdx.x, nt_ = blockDim.x;
   const int np = (n + 1) & ~1;
   const int half = np / 2;
@@ -257,7 +260,7 @@ __device__ bool jacobi_eigh(double* a, int lda, double* u, int ldu, int n, const
     const int i = idx % n, j = idx / n;
     const double v = a[i + j * lda];
     fro = fma(v, v, fro);
-    u[i + j * ldu] = i == j ? 1.0 : 0.0;
+    if (want_vectors) u[i + j * ldu] = i == j ? 1.0 : 0.0;
   }
   if (np > n) {  // padding index: zero row/column, never rotated (a_pq == 0 rule)
     for (int i = tid; i < np; i += nt_) {
@@ -331,7 +334,7 @@ __device__ bool jacobi_eigh(double* a, int lda, double* u, int ldu, int n, const
             const double aip = a[i + p * lda], aiq = a[i + q * lda];
             a[i + p * lda] = cs * aip - sn * aiq;
             a[i + q * lda] = sn * aip + cs * aiq;
-            if (i < n) {
+            if (want_vectors && i < n) {
               const double uip = u[i + p * ldu], uiq = u[i + q * ldu];
               u[i + p * ldu] = cs * uip - sn * uiq;
               u[i + q * ldu] = sn * uip + cs * uiq;
@@ -510,7 +513,7 @@ __global__ void __launch_bounds__(kJacobiMaxThreads)
   if (want_sigma) {
     for (int idx = tid; idx < n * n; idx += nt_) a[idx % n + (idx / n) * L.lda] = c[idx];
     __syncthreads();
-    ok = jacobi_eigh(a, L.lda, u, L.ldu, n, js);
+    ok = jacobi_eigh(a, L.lda, u, L.ldu, n, js, false);
     if (!ok && tid == 0) raise_status(status, SQB_E_NO_CONVERGENCE, -1);
     for (int j = tid; j < n; j += nt_)
       sigma[j] = sqrt(fmax(a[js.perm[j] + js.perm[j] * L.lda], 0.0));
