@@ -61,6 +61,10 @@ struct GramCfg {
   static constexpr int kPlainP[8] = {120, 72, kCtas == 2 ? 24 : 40, kCtas == 2 ? 24 : 40, 40, 24, 24, 24};
   static constexpr int kMultP[8] = {112, kCtas == 2 ? 32 : 64, kCtas == 2 ? 16 : 48, kCtas == 2 ? 16 : 32, 32, 16, 16, 16};
   static constexpr int kBlockedP[8] = {64, kCtas == 2 ? 32 : 64, kCtas == 2 ? 16 : 48, kCtas == 2 ? 16 : 32, 32, 16, 16, 16};  // == 0 (mod 16): pitch P + 4
+  // row groups unrolled in the plain pass - measured per tile count (the DMMA issue order that ptxas derives
+  // from it is worth -29 % .. +34 %): 6 and 8 tiles want pairs, everything else the whole panel
+  // (two to four remainder columns: pairs again, except at 18 columns - measured)
+  static constexpr int kPlainUnroll = (NB == 6 || NB == 8 || R >= 3 || (R == 2 && NB >= 3)) ? 2 : 15;
   static constexpr int kMultUnroll = NB == 1 ? 2 : (NB == 2 ? 4 : (NB == 3 ? (kCtas == 2 ? 2 : 3) : 1));  // measured: no gain from 32 columns on
   static constexpr int kSolveUnroll = NB <= 2 ? 4 : (kCtas == 2 ? 2 : (NB == 3 ? 3 : (NB == 4 ? 4 : (NB <= 6 ? 2 : 1))));  // row groups solved together
   static constexpr int P =
@@ -234,7 +238,7 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
     }
 
     if (OP == OP_PLAIN) {
-#pragma unroll 2
+#pragma unroll(Cfg::kPlainUnroll)
       for (int t = 0; t < P / 8; ++t) {
         double2 a[NB];
 #pragma unroll
