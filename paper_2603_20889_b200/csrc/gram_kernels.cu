@@ -65,8 +65,8 @@ struct GramCfg {
   // from it is worth -29 % .. +34 %): 6 and 8 tiles want pairs, everything else the whole panel
   // (two to four remainder columns: pairs again, except at 18 columns - measured)
   static constexpr int kPlainUnroll = (NB == 6 || NB == 8 || R >= 3 || (R == 2 && NB >= 3)) ? 2 : 15;
-  static constexpr int kMultUnroll = NB == 1 ? 2 : (NB == 2 ? 4 : (NB == 3 ? (kCtas == 2 ? 2 : 3) : 1));  // measured: no gain from 32 columns on
-  static constexpr int kSolveUnroll = NB <= 2 ? 4 : (kCtas == 2 ? 2 : (NB == 3 ? 3 : (NB == 4 ? 4 : (NB <= 6 ? 2 : 1))));  // row groups solved together
+  static constexpr int kMultUnroll = NB == 2 ? 4 : (NB == 3 ? (kCtas == 2 ? 2 : 3) : 2);  // row groups multiplied together (measured per tile count)
+  static constexpr int kSolveUnroll = NB <= 2 ? 4 : (kCtas == 2 ? 2 : (NB == 3 ? 3 : (NB == 4 ? 4 : (NB == 5 ? 4 : 2))));  // row groups solved together
   static constexpr int P =
       kBlockedSolve ? kBlockedP[NB - 1] : (OP == OP_PLAIN ? kPlainP[NB - 1] : kMultP[NB - 1]);
   // Blocked solve: the stage is read with the transposed LDS.64 pattern (DMMA B operands) AND read / written
