@@ -56,7 +56,10 @@ struct GramCfg {
 #ifndef SQB_GRAM_2CTA_NB2
 #define SQB_GRAM_2CTA_NB2 1
 #endif
-  static constexpr int kCtas = ((SQB_GRAM_2CTA && (OP == OP_PLAIN || SQB_GRAM_2CTA_ALL) && (NB == 3 || NB == 4)) ||
+  // measured: the plain pass wants two CTAs per SM at 3 and 4 tiles, the fused passes at 2 and 4 tiles (at 3
+  // tiles one CTA with taller panels and, for the solve, the swizzled stage is 3-5 % faster)
+  static constexpr int kCtas = ((SQB_GRAM_2CTA && ((OP == OP_PLAIN && (NB == 3 || NB == 4)) ||
+                                                   (OP != OP_PLAIN && SQB_GRAM_2CTA_ALL && NB == 4))) ||
                                 (SQB_GRAM_2CTA_NB2 && OP != OP_PLAIN && NB == 2)) ? 2 : 1;
   static constexpr int kPlainP[8] = {120, 72, kCtas == 2 ? 24 : 40, kCtas == 2 ? 24 : 40, 40, 24, 24, 24};
   static constexpr int kMultP[8] = {112, kCtas == 2 ? 32 : 64, kCtas == 2 ? 16 : 48, kCtas == 2 ? 16 : 32, 32, 16, 16, 16};
@@ -596,7 +599,8 @@ int gram_ctas_per_sm(int n, int op) {
   if (gram_use_thread(n, op)) return gram_thread_ctas_per_sm(n, op);
   const int nb = gram_remainder_variant(n, op) ? n / 8 : (n + 7) / 8;
   if (SQB_GRAM_2CTA_NB2 && op != OP_PLAIN && nb == 2) return 2;
-  return (SQB_GRAM_2CTA && (op == OP_PLAIN || SQB_GRAM_2CTA_ALL) && (nb == 3 || nb == 4)) ? 2 : 1;
+  if (op != OP_PLAIN) return (SQB_GRAM_2CTA && SQB_GRAM_2CTA_ALL && nb == 4) ? 2 : 1;
+  return (SQB_GRAM_2CTA && (nb == 3 || nb == 4)) ? 2 : 1;
 }
 
 }  // namespace sqb
