@@ -167,7 +167,7 @@ struct Small {
 
 int small_slots(sqb_context* ctx, int n, Small* s) {
   const size_t nn = static_cast<size_t>(n) * n;
-  const size_t want = 10 * nn + 4 * n + (nn + 3 * n + 16) + 8;
+  const size_t want = 10 * nn + 4 * n + small_scratch_doubles(n) + 8;
   SQB_TRY(grow(&ctx->small, &ctx->small_doubles, want));
   double* p = ctx->small;
   s->c1 = p; p += nn;

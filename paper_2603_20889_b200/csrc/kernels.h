@@ -142,6 +142,8 @@ cudaError_t launch_cholesky(const double* c, int n, double* r, StatusWord* statu
 // U = R^-1 (n x n column-major) for any n; scratch_rowmajor: n x n doubles
 cudaError_t launch_rinv_global(const double* r, int n, double* scratch_rowmajor, double* u, StatusWord* status,
                                cudaStream_t stream);
+// doubles of global scratch launch_eigh / launch_svqb_pass / the Cholesky kernels need at n columns
+size_t small_scratch_doubles(int n);
 cudaError_t launch_eigh(const double* c, int n, double* values, double* vectors, double* scratch,
                         StatusWord* status, cudaStream_t stream);
 // scratch: at least n*(n+1) + 2*n doubles of device memory (U beyond 64 columns, the two diagonal scalings)

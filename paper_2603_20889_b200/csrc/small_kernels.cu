@@ -8,6 +8,7 @@
 //   small_multiply      reference small_multiply      (src/small.cpp:22-32)
 //   backsolve_kernel    reference solve_lstsq tail    (src/lstsq.cpp:44-59)
 //   apply_rinv_kernel   reference reconstruct_q       (src/gram_qr.cpp:193-221)
+#include <algorithm>
 #include <cfloat>
 
 #include "kernels.h"
@@ -26,6 +27,7 @@ inline int jacobi_threads(int n) {
   return warps <= 8 ? 256 : (warps <= 16 ? 512 : (warps <= 24 ? 768 : 1024));
 }
 constexpr double kEps = 2.220446049250313e-16;  // std::numeric_limits<double>::epsilon()
+constexpr int kJacobiMaxSweeps = 30;               // gram_qr.cpp:69
 
 // ------------------------------------------------------------------------------------------------
 // Cholesky: right-looking, upper factor R^T R = C.  Arithmetic per entry is the reference's
@@ -196,15 +198,26 @@ __global__ void __launch_bounds__(256)
 // Symmetric eigensolver: Jacobi with the reference's rotation formulas, skip rule (a_pq == 0),
 // stopping test off(A) <= 10*n*eps*|C|_F checked once per sweep, 30-sweep cap and stable
 // descending sort (gram_qr.cpp:60-121).  The reference sweeps cyclic-by-row, one rotation at a
-// time; here the n/2 disjoint rotations of a round-robin round are applied together (column
-// phase, row phase; one warp per pair, two CTA barriers per round).
-// `a` (np x lda, np = n rounded up to even) and `u` (n x ldu) are CTA-visible scratch.
-// Returns false when the sweep cap is hit.  On return perm[j] = source column of output j.
+// time; here the n/2 disjoint rotations J = J_1 ... J_{n/2} of a round-robin round are applied together
+// as one two-sided update A <- J^T A J.
+//
+// One CTA, everything in shared memory:
+//   * A is kept as its packed upper triangle (a(i, j), i <= j, at j (j + 1) / 2 + i): 66 KB at 128 columns,
+//     which leaves room for the full U (132 KB) beside it - no global-memory U, no second pass.
+//   * A round = (1) one THREAD per pair derives (c, s) and writes the exact 2 x 2 result of its own diagonal
+//     block (gram_qr.cpp:84-87); (2) after a barrier one thread per unordered PAIR OF PAIRS (P, Q) updates the
+//     2 x 2 block A[P, Q] <- J_P^T (A[P, Q] J_Q) - four loads, 16 flops, four stores, each entry of the
+//     triangle touched once - while the warps rotate the columns of U; (3) barrier.
+//   The former column-phase / row-phase formulation over a full square A touched every entry twice with
+//   ~8 integer instructions per FMA and was ISSUE bound: 23.6 M warp instructions, 10 300 clk per round at
+//   n = 128 (ncu, round 2); this one issues about a quarter of that.
+// Returns false when the sweep cap is hit.  On return lam[j] = eigenvalue at index j, perm[j] = source
+// index of output j, and column perm[j] of U the eigenvector.
 // ------------------------------------------------------------------------------------------------
 // The rotation scalars are a serial chain of two divisions, a square root and a reciprocal square root
-// per round; the IEEE software sequences for those cost ~3000 clk per round, i.e. most of the solver.
-// MUFU seed + two Newton steps each (<= 1-2 ulp) take a tenth of that; the eigen-decomposition is
-// compared through its invariants, never bitwise.
+// per round; the IEEE software sequences for those cost ~3000 clk per round.  MUFU seed + two Newton steps
+// each (<= 1-2 ulp) take a tenth of that; the eigen-decomposition is compared through its invariants,
+// never bitwise.
 __device__ __forceinline__ double fast_rcp(double x) {
   double z;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(z) : "d"(x));
@@ -223,71 +236,85 @@ __device__ __forceinline__ double fast_rsqrt(double x) {  // x in [1, 1e200]
 }
 
 struct JacobiScratch {
-  double* cs;    // np/2
-  double* sn;    // np/2
-  double* dpp;   // np/2
-  double* dqq;   // np/2
-  int* pp;       // np/2
-  int* qq;       // np/2
-  double* red;   // kJacobiMaxThreads
-  int* perm;     // n
+  double* cs;      // np/2
+  double* sn;      // np/2
+  int2* pq;        // np/2: the (p, q), p < q, of pair t in this round
+  double* red;     // 32
+  int* perm;       // n
+  double* lam;     // n: the eigenvalues by index (diagonal of the converged A)
+  unsigned* blk;   // (np/2)(np/2 - 1)/2: the unordered pairs (tP < tQ) of pair slots, (tP << 16) | tQ
 };
 
+__device__ __forceinline__ int tri_at(int i, int j) {  // packed upper triangle, either order
+  const int hi = max(i, j), lo = min(i, j);
+  return ((hi * (hi + 1)) >> 1) + lo;
+}
+
 __device__ double block_sum(double v, double* red) {
-  const int tid = threadIdx.x, nt_ = blockDim.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   __syncthreads();
-  red[tid] = v;
+  if (lane == 0) red[warp] = v;
   __syncthreads();
-  for (int s = nt_ / 2; s > 0; s >>= 1) {
-    if (tid < s) red[tid] += red[tid + s];
-    __syncthreads();
-  }
-  const double out = red[0];
+  double out = 0.0;
+  for (int w = 0; w < nw; ++w) out += red[w];  // every thread, same order: a CTA-uniform result
   __syncthreads();
   return out;
 }
 
-// want_vectors = false skips every access to U (the sigma eigensolve of an SVQB pass only needs the eigenvalues;
-// beyond 64 columns U lives in global memory and is the larger half of a round's traffic).
-__device__ bool jacobi_eigh(double* a, int lda, double* u, int ldu, int n, const JacobiScratch& js,
-                            bool want_vectors = true) {
+// want_vectors = false skips U altogether (the sigma eigensolve of an SVQB pass only needs the eigenvalues).
+// `a`: packed upper triangle of order np = n rounded up to even, entries (i <= j < n) filled by the caller.
+__device__ bool jacobi_eigh(double* a, double* u, int ldu, int n, const JacobiScratch& js, bool want_vectors = true) {
   const int tid = threadIdx.x, nt_ = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31, nwarps = nt_ >> 5;
   const int np = (n + 1) & ~1;
   const int half = np / 2;
+  const int nblk = half * (half - 1) / 2;
+
+  // the block list: the strict upper triangle of the half x half slot grid, folded into half/2 rows of
+  // half - 1 entries (row r of the triangle together with row half - 1 - r)
+  for (int k = tid; k < nblk; k += nt_) {
+    const int r = k / (half - 1), c = k % (half - 1);
+    int tp, tq;
+    if (c < half - 1 - r) {
+      tp = r;
+      tq = r + 1 + c;
+    } else {
+      tp = half - 1 - r;
+      tq = tp + 1 + (c - (half - 1 - r));
+    }
+    js.blk[k] = (static_cast<unsigned>(tp) << 16) | static_cast<unsigned>(tq);
+  }
+  if (np > n) {  // padding index n: zero row/column, never rotated (a_pq == 0 rule)
+    for (int i = tid; i < np; i += nt_) a[tri_at(i, n)] = 0.0;
+  }
   // |C|_F and identity U
   double fro = 0.0;
   for (int idx = tid; idx < n * n; idx += nt_) {
     const int i = idx % n, j = idx / n;
-    const double v = a[i + j * lda];
-    fro = fma(v, v, fro);
-    if (want_vectors) u[i + j * ldu] = i == j ? 1.0 : 0.0;
-  }
-  if (np > n) {  // padding index: zero row/column, never rotated (a_pq == 0 rule)
-    for (int i = tid; i < np; i += nt_) {
-      a[i + n * lda] = 0.0;
-      a[n + i * lda] = 0.0;
+    if (i <= j) {
+      const double v = a[tri_at(i, j)];
+      fro = fma(i == j ? v : 2.0 * v, v, fro);
     }
+    if (want_vectors) u[i + j * ldu] = i == j ? 1.0 : 0.0;
   }
   const double thr = 10.0 * static_cast<double>(n) * kEps * sqrt(block_sum(fro, js.red));
 
   auto offdiag = [&]() {
     double s = 0.0;
-    for (int idx = tid; idx < n * n; idx += nt_) {
-      const int i = idx % n, j = idx / n;
-      if (i < j) s = fma(a[i + j * lda], a[i + j * lda], s);
+    for (int j = 1 + warp; j < n; j += nwarps) {
+      const double* col = a + ((j * (j + 1)) >> 1);
+      for (int i = lane; i < j; i += 32) s = fma(col[i], col[i], s);
     }
     return sqrt(2.0 * block_sum(s, js.red));
   };
 
   bool converged = offdiag() <= thr;
-  for (int sweep = 0; sweep < 30 && !converged; ++sweep) {
+  for (int sweep = 0; sweep < kJacobiMaxSweeps && !converged; ++sweep) {
     for (int step = 0; step < np - 1; ++step) {
-      // A WARP owns a pair of the round: every lane derives the rotation itself (no parameter
-      // exchange, no barrier between "parameters" and "columns"), then the lanes share the rows.
-      // Pairs of one round are disjoint, and the entries a_pp, a_qq, a_pq a warp reads here are only
-      // ever written by that warp (columns) or after the CTA barrier (rows).
-      const int warp = tid >> 5, lane = tid & 31, nwarps = nt_ >> 5;
-      for (int t = warp; t < half; t += nwarps) {
+      // (1) rotation of pair slot t (round-robin: slot 0 keeps index np - 1)
+      if (tid < half) {
+        const int t = tid;
         int x, y;
         if (t == 0) {
           x = np - 1;
@@ -297,83 +324,79 @@ __device__ bool jacobi_eigh(double* a, int lda, double* u, int ldu, int n, const
           y = (step - t + (np - 1)) % (np - 1);
         }
         const int p = min(x, y), q = max(x, y);
-        const double apq = a[p + q * lda];
-        double cs = 1.0, sn = 0.0, npp = 0.0, nqq = 0.0;
-        const bool rot = apq != 0.0;
-        if (rot) {
-          const double app = a[p + p * lda], aqq = a[q + q * lda];
+        const int ipp = ((p * (p + 1)) >> 1) + p, iqq = ((q * (q + 1)) >> 1) + q, ipq = ((q * (q + 1)) >> 1) + p;
+        const double apq = a[ipq];
+        double cs = 1.0, sn = 0.0;
+        if (apq != 0.0) {
+          const double app = a[ipp], aqq = a[iqq];
           const double theta = (aqq - app) * fast_rcp(2.0 * apq);
           const double ath = fabs(theta);
           double tt;
           if (ath < 1e100) {
             const double r2 = fma(theta, theta, 1.0);
-            const double y = fast_rsqrt(r2);
-            double sq = r2 * y;
-            sq = fma(fma(-sq, sq, r2), 0.5 * y, sq);  // sqrt(1 + theta^2), residual-corrected
+            const double y2 = fast_rsqrt(r2);
+            double sq = r2 * y2;
+            sq = fma(fma(-sq, sq, r2), 0.5 * y2, sq);  // sqrt(1 + theta^2), residual-corrected
             tt = (theta >= 0.0 ? 1.0 : -1.0) * fast_rcp(ath + sq);
           } else {
             tt = 0.5 / theta;  // sqrt(1 + theta^2) == |theta| in working precision (also theta = +-inf)
           }
           cs = fast_rsqrt(fma(tt, tt, 1.0));
           sn = tt * cs;
-          npp = app - tt * apq;
-          nqq = aqq + tt * apq;
+          a[ipp] = app - tt * apq;  // the exact 2 x 2 results (gram_qr.cpp:84-87)
+          a[iqq] = aqq + tt * apq;
+          a[ipq] = 0.0;
         }
-        if (lane == 0) {
-          js.cs[t] = cs;
-          js.sn[t] = sn;
-          js.dpp[t] = npp;
-          js.dqq[t] = nqq;
-          js.pp[t] = rot ? p : -1;
-          js.qq[t] = q;
-        }
-        __syncwarp();  // every lane has read a_pp, a_qq, a_pq before the columns change
-        if (rot) {
-          // columns  A <- A J,  U <- U J
-          for (int i = lane; i < np; i += 32) {
-            const double aip = a[i + p * lda], aiq = a[i + q * lda];
-            a[i + p * lda] = cs * aip - sn * aiq;
-            a[i + q * lda] = sn * aip + cs * aiq;
-            if (want_vectors && i < n) {
-              const double uip = u[i + p * ldu], uiq = u[i + q * ldu];
-              u[i + p * ldu] = cs * uip - sn * uiq;
-              u[i + q * ldu] = sn * uip + cs * uiq;
-            }
-          }
-        }
+        js.cs[t] = cs;
+        js.sn[t] = sn;
+        js.pq[t] = make_int2(p, q);
       }
       __syncthreads();
-      // rows  A <- J^T A, then the exact 2x2 results (gram_qr.cpp:84-87)
-      for (int t = warp; t < half; t += nwarps) {
-        const int p = js.pp[t];
-        if (p < 0) continue;
-        const int q = js.qq[t];
-        const double cs = js.cs[t], sn = js.sn[t];
-        for (int j = lane; j < np; j += 32) {
-          const double apj = a[p + j * lda], aqj = a[q + j * lda];
-          a[p + j * lda] = cs * apj - sn * aqj;
-          a[q + j * lda] = sn * apj + cs * aqj;
-        }
-        __syncwarp();
-        if (lane == 0) {
-          a[p + p * lda] = js.dpp[t];
-          a[q + q * lda] = js.dqq[t];
-          a[p + q * lda] = 0.0;
-          a[q + p * lda] = 0.0;
+      // (2a) off-diagonal blocks: A[P, Q] <- J_P^T (A[P, Q] J_Q).  An unrotated pair has (c, s) = (1, 0): exact.
+      for (int k = tid; k < nblk; k += nt_) {
+        const unsigned e = js.blk[k];
+        const int tp = e >> 16, tq = e & 0xffffu;
+        const int2 P = js.pq[tp], Q = js.pq[tq];
+        const double cp = js.cs[tp], sp = js.sn[tp], cq = js.cs[tq], sq = js.sn[tq];
+        const int i00 = tri_at(P.x, Q.x), i01 = tri_at(P.x, Q.y), i10 = tri_at(P.y, Q.x), i11 = tri_at(P.y, Q.y);
+        const double a00 = a[i00], a01 = a[i01], a10 = a[i10], a11 = a[i11];
+        const double b00 = cq * a00 - sq * a01, b01 = sq * a00 + cq * a01;  // columns: . J_Q
+        const double b10 = cq * a10 - sq * a11, b11 = sq * a10 + cq * a11;
+        a[i00] = cp * b00 - sp * b10;                                       // rows: J_P^T .
+        a[i10] = sp * b00 + cp * b10;
+        a[i01] = cp * b01 - sp * b11;
+        a[i11] = sp * b01 + cp * b11;
+      }
+      // (2b) U <- U J: a warp per pair, lanes over the rows
+      if (want_vectors) {
+        for (int t = warp; t < half; t += nwarps) {
+          const double cs = js.cs[t], sn = js.sn[t];
+          if (sn == 0.0) continue;  // identity (this also keeps the padding index out of U)
+          const int2 P = js.pq[t];
+          double* up = u + P.x * ldu;
+          double* uq = u + P.y * ldu;
+          for (int i = lane; i < n; i += 32) {
+            const double uip = up[i], uiq = uq[i];
+            up[i] = cs * uip - sn * uiq;
+            uq[i] = sn * uip + cs * uiq;
+          }
         }
       }
       __syncthreads();
     }
     converged = offdiag() <= thr;
   }
-  // stable descending rank (gram_qr.cpp:107-110)
-  for (int j = tid; j < n; j += nt_) js.perm[j] = j;
+  // eigenvalues by index, then the stable descending rank (gram_qr.cpp:107-110)
+  for (int j = tid; j < n; j += nt_) {
+    js.lam[j] = a[((j * (j + 1)) >> 1) + j];
+    js.perm[j] = j;
+  }
   __syncthreads();
   for (int j = tid; j < n; j += nt_) {
-    const double lj = a[j + j * lda];
+    const double lj = js.lam[j];
     int rank = 0;
     for (int i = 0; i < n; ++i) {
-      const double li = a[i + i * lda];
+      const double li = js.lam[i];
       rank += (li > lj) || (li == lj && i < j);
     }
     js.perm[rank] = j;
@@ -383,58 +406,57 @@ __device__ bool jacobi_eigh(double* a, int lda, double* u, int ldu, int n, const
 }
 
 struct SmallLayout {
-  int lda, ldu;
+  int ldu;
   size_t a_off, u_off, misc_off, total_doubles;
-  bool u_in_smem;
 };
 
 __host__ __device__ inline SmallLayout small_layout(int n) {
   SmallLayout L;
   const int np = (n + 1) & ~1;
-  L.lda = np + 1;
+  const int half = np / 2;
   L.ldu = n + 1;
   L.a_off = 0;
-  size_t off = static_cast<size_t>(np) * L.lda;
-  L.u_in_smem = n <= 64;
+  size_t off = (static_cast<size_t>(np) * (np + 1) / 2 + 1) & ~static_cast<size_t>(1);
   L.u_off = off;
-  if (L.u_in_smem) off += static_cast<size_t>(n) * L.ldu;
+  off += (static_cast<size_t>(n) * L.ldu + 1) & ~static_cast<size_t>(1);
   L.misc_off = off;
-  // cs, sn, dpp, dqq (np/2 each), pp, qq (np/2 ints each -> np/2 doubles), red, perm (n ints)
-  off += 4 * (np / 2) + (np / 2) + kJacobiMaxThreads + (n + 1) / 2 + 4;
+  // cs, sn, pq (half each), red (32), perm (n ints), lam (n), blk (half (half - 1) / 2 unsigned)
+  off += 3 * half + 32 + (n + 1) / 2 + 2 + np + (static_cast<size_t>(half) * (half - 1) / 2 + 1) / 2 + 2;
   L.total_doubles = off;
   return L;
 }
 
 __device__ JacobiScratch carve_scratch(double* sm, const SmallLayout& L, int n) {
   const int np = (n + 1) & ~1;
+  const int half = np / 2;
   JacobiScratch js;
   double* p = sm + L.misc_off;
-  js.cs = p; p += np / 2;
-  js.sn = p; p += np / 2;
-  js.dpp = p; p += np / 2;
-  js.dqq = p; p += np / 2;
-  js.pp = reinterpret_cast<int*>(p);
-  js.qq = js.pp + np / 2;
-  p += np / 2;
-  js.red = p; p += kJacobiMaxThreads;
-  js.perm = reinterpret_cast<int*>(p);
+  js.cs = p; p += half;
+  js.sn = p; p += half;
+  js.pq = reinterpret_cast<int2*>(p); p += half;
+  js.red = p; p += 32;
+  js.perm = reinterpret_cast<int*>(p); p += (n + 1) / 2 + 2;
+  js.lam = p; p += np;
+  js.blk = reinterpret_cast<unsigned*>(p);
   return js;
 }
 
 __global__ void __launch_bounds__(kJacobiMaxThreads)
-    eigh_kernel(const double* __restrict__ c, int n, double* values, double* vectors,
-                double* gscratch, StatusWord* status) {
+    eigh_kernel(const double* __restrict__ c, int n, double* values, double* vectors, StatusWord* status) {
   extern __shared__ __align__(16) double sm[];
   const SmallLayout L = small_layout(n);
   double* a = sm + L.a_off;
-  double* u = L.u_in_smem ? sm + L.u_off : gscratch;
+  double* u = sm + L.u_off;
   const JacobiScratch js = carve_scratch(sm, L, n);
   const int tid = threadIdx.x, nt_ = blockDim.x;
-  for (int idx = tid; idx < n * n; idx += nt_) a[idx % n + (idx / n) * L.lda] = c[idx];
+  for (int idx = tid; idx < n * n; idx += nt_) {
+    const int i = idx % n, j = idx / n;
+    if (i <= j) a[tri_at(i, j)] = c[idx];
+  }
   __syncthreads();
-  const bool ok = jacobi_eigh(a, L.lda, u, L.ldu, n, js);
+  const bool ok = jacobi_eigh(a, u, L.ldu, n, js);
   if (!ok && tid == 0) raise_status(status, SQB_E_NO_CONVERGENCE, -1);
-  for (int j = tid; j < n; j += nt_) values[j] = a[js.perm[j] + js.perm[j] * L.lda];
+  for (int j = tid; j < n; j += nt_) values[j] = js.lam[js.perm[j]];
   for (int idx = tid; idx < n * n; idx += nt_) {
     const int i = idx % n, j = idx / n;
     vectors[idx] = u[i + js.perm[j] * L.ldu];
@@ -444,20 +466,33 @@ __global__ void __launch_bounds__(kJacobiMaxThreads)
 // One SVQB pass on a Gram matrix (gram_qr.cpp:133-176): D = diag(C)^-1/2 (1 for zero columns),
 // eigen-decomposition of D C D, rank = #{lambda >= 10 n eps lambda_max}, B = D U L^-1/2,
 // Z = L^1/2 U^T D^-1 with truncated columns/rows exactly zero; sigma = sqrt(max(eig(C), 0)) from a
-// second eigen-decomposition of the unscaled Gram matrix.
+// second eigen-decomposition of the unscaled Gram matrix - independent of the first, so it runs beside it
+// as the launch's second CTA (eigenvalues only).
 __global__ void __launch_bounds__(kJacobiMaxThreads)
     svqb_pass_kernel(const double* __restrict__ c, int n, double* bmat, double* z, double* sigma,
-                     long long* rank_out, int want_sigma, double* gscratch, StatusWord* status) {
+                     long long* rank_out, double* gscratch, StatusWord* status) {
   extern __shared__ __align__(16) double sm[];
   const SmallLayout L = small_layout(n);
   double* a = sm + L.a_off;
-  double* u = L.u_in_smem ? sm + L.u_off : gscratch;
-  double* ds = gscratch + static_cast<size_t>(n) * (n + 1);   // n
-  double* dsi = ds + n;                                       // n
+  double* u = sm + L.u_off;
+  double* ds = gscratch;      // n
+  double* dsi = ds + n;       // n
   const JacobiScratch js = carve_scratch(sm, L, n);
   __shared__ int rank_s;
   __shared__ int fail_s;
   const int tid = threadIdx.x, nt_ = blockDim.x;
+
+  if (blockIdx.x == 1) {
+    for (int idx = tid; idx < n * n; idx += nt_) {
+      const int i = idx % n, j = idx / n;
+      if (i <= j) a[tri_at(i, j)] = c[idx];
+    }
+    __syncthreads();
+    const bool sok = jacobi_eigh(a, u, L.ldu, n, js, false);
+    if (!sok && tid == 0) raise_status(status, SQB_E_NO_CONVERGENCE, -1);
+    for (int j = tid; j < n; j += nt_) sigma[j] = sqrt(fmax(js.lam[js.perm[j]], 0.0));
+    return;
+  }
 
   for (int j = tid; j < n; j += nt_) {
     const double d = c[j + j * n];
@@ -468,23 +503,23 @@ __global__ void __launch_bounds__(kJacobiMaxThreads)
   __syncthreads();
   for (int idx = tid; idx < n * n; idx += nt_) {
     const int i = idx % n, j = idx / n;
-    a[i + j * L.lda] = c[idx] * ds[i] * ds[j];
+    if (i <= j) a[tri_at(i, j)] = c[idx] * ds[i] * ds[j];
   }
   __syncthreads();
-  bool ok = jacobi_eigh(a, L.lda, u, L.ldu, n, js);
+  const bool ok = jacobi_eigh(a, u, L.ldu, n, js);
   if (tid == 0) {
     int rank = 0;
     if (!ok) {
       raise_status(status, SQB_E_NO_CONVERGENCE, -1);
       fail_s = 1;
     } else {
-      const double lmax = a[js.perm[0] + js.perm[0] * L.lda];
+      const double lmax = js.lam[js.perm[0]];
       if (!(lmax > 0.0)) {
         raise_status(status, SQB_E_ZERO_MATRIX, -1);
         fail_s = 1;
       } else {
         const double tol = 10.0 * static_cast<double>(n) * kEps;
-        while (rank < n && a[js.perm[rank] + js.perm[rank] * L.lda] >= tol * lmax) ++rank;
+        while (rank < n && js.lam[js.perm[rank]] >= tol * lmax) ++rank;
         if (rank == 0) {
           raise_status(status, SQB_E_ZERO_MATRIX, -1);
           fail_s = 1;
@@ -501,22 +536,13 @@ __global__ void __launch_bounds__(kJacobiMaxThreads)
     double bv = 0.0, zv = 0.0;
     if (j < rank && !fail_s) {
       const int src = js.perm[j];
-      const double lam = a[src + src * L.lda];
+      const double lam = js.lam[src];
       const double uij = u[i + src * L.ldu];
       bv = ds[i] * uij * (1.0 / sqrt(lam));
       zv = sqrt(lam) * uij * dsi[i];
     }
     bmat[i + j * n] = bv;   // B(i,j)
     z[j + i * n] = zv;      // Z(j,i)
-  }
-  __syncthreads();
-  if (want_sigma) {
-    for (int idx = tid; idx < n * n; idx += nt_) a[idx % n + (idx / n) * L.lda] = c[idx];
-    __syncthreads();
-    ok = jacobi_eigh(a, L.lda, u, L.ldu, n, js, false);
-    if (!ok && tid == 0) raise_status(status, SQB_E_NO_CONVERGENCE, -1);
-    for (int j = tid; j < n; j += nt_)
-      sigma[j] = sqrt(fmax(a[js.perm[j] + js.perm[j] * L.lda], 0.0));
   }
 }
 
@@ -698,12 +724,18 @@ cudaError_t launch_rinv_global(const double* r, int n, double* scratch_rowmajor,
   return cudaGetLastError();
 }
 
+size_t small_scratch_doubles(int n) {
+  const size_t nn = static_cast<size_t>(n) * n;
+  return nn + 3 * static_cast<size_t>(n) + 16;
+}
+
 cudaError_t launch_eigh(const double* c, int n, double* values, double* vectors, double* scratch,
                         StatusWord* status, cudaStream_t stream) {
   const size_t bytes = small_smem_bytes(n);
   cudaError_t e = opt_in_smem(eigh_kernel, bytes);
   if (e != cudaSuccess) return e;
-  eigh_kernel<<<1, jacobi_threads(n), bytes, stream>>>(c, n, values, vectors, scratch, status);
+  (void)scratch;
+  eigh_kernel<<<1, jacobi_threads(n), bytes, stream>>>(c, n, values, vectors, status);
   return cudaGetLastError();
 }
 
@@ -713,8 +745,8 @@ cudaError_t launch_svqb_pass(const double* c, int n, double* b, double* z, doubl
   const size_t bytes = small_smem_bytes(n);
   cudaError_t e = opt_in_smem(svqb_pass_kernel, bytes);
   if (e != cudaSuccess) return e;
-  svqb_pass_kernel<<<1, jacobi_threads(n), bytes, stream>>>(c, n, b, z, sigma, rank, want_sigma, scratch,
-                                                        status);
+  svqb_pass_kernel<<<want_sigma ? 2 : 1, jacobi_threads(n), bytes, stream>>>(c, n, b, z, sigma, rank, scratch,
+                                                                          status);
   return cudaGetLastError();
 }
 

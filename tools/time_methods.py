@@ -1,10 +1,11 @@
 """Quick device-side timing of one method over a list of column counts.
 python tools/time_methods.py METHOD n1,n2,... [LOG2_ELEMS] [REPS] [KERNEL]   (m = 2^LOG2_ELEMS / n rows;
 KERNEL = auto | thread | fold | mma forces a TSQR kernel family)"""
+import os
 import sys
 from pathlib import Path
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.insert(0, os.environ.get("SQB_PKG_ROOT", str(Path(__file__).resolve().parents[1])))  # A/B: an older build
 import torch  # noqa: E402
 import paper_2603_20889_b200 as sq  # noqa: E402
 
