@@ -54,6 +54,12 @@ prof3() { # the fused wide sweeps (64 < n <= 128): second streaming launch of ch
 prof3 gram_wide_solve_n128 cholqr2
 prof3 gram_wide_multiply_n128 svqb2
 prof gram_wide2_gemm_n256 gram_wide_fused cholqr2 256 22
+ncu --set full --clock-control none --import-source on -k regex:eigh_kernel -c 1 -o $O/${TAG}_eigh_n128 python tools/time_small.py 128 1 > /dev/null 2>&1
+ncu -i $O/${TAG}_eigh_n128.ncu-rep --page raw --csv > $O/${TAG}_eigh_n128.raw.csv 2>/dev/null
+ncu -i $O/${TAG}_eigh_n128.ncu-rep --page source --csv > $O/${TAG}_eigh_n128.source.csv 2>/dev/null
+python tools/src_csv.py $O/${TAG}_eigh_n128.source.csv --regions > $O/${TAG}_eigh_n128.source_summary.txt 2>&1
+rm -f $O/${TAG}_eigh_n128.ncu-rep $O/${TAG}_eigh_n128.source.csv
+python tools/time_small.py 8,16,32,64,96,128,256 5 > $O/${TAG}_small.txt 2>&1
 python tools/time_gram_wide.py 24 > $O/${TAG}_wide.txt 2>&1
 ALLN=$(seq -s, 1 64)
 for meth in tsqr cholqr2 svqb2 tsmttsm; do python tools/time_methods.py $meth $ALLN 31 5 >> $O/${TAG}_all_n.txt 2>&1; done
