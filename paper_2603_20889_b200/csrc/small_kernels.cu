@@ -20,12 +20,9 @@ namespace {
 constexpr int kSmallThreads = 256;
 // The Jacobi kernels scale their thread count with n: a round of the 64 x 64 problem rotates 2 x 2048
 // column / row entries of A and U, which 256 threads walk in 8 trips between CTA barriers.
-constexpr int kJacobiMaxThreads = 1024;
-// one warp per rotation pair of a round (n/2 pairs), at most 32 warps
-inline int jacobi_threads(int n) {
-  const int warps = (n + 1) / 2;
-  return warps <= 8 ? 256 : (warps <= 16 ? 512 : (warps <= 24 ? 768 : 1024));
-}
+constexpr int kJacobiMaxThreads = 512;
+// a thread per pair of index groups (<= 496 at 128 columns) and a warp per group (<= 32), at 128 registers
+inline int jacobi_threads(int n) { return n <= 32 ? 256 : 512; }
 constexpr double kEps = 2.220446049250313e-16;  // std::numeric_limits<double>::epsilon()
 constexpr int kJacobiMaxSweeps = 30;               // gram_qr.cpp:69
 
@@ -198,26 +195,31 @@ __global__ void __launch_bounds__(256)
 // Symmetric eigensolver: Jacobi with the reference's rotation formulas, skip rule (a_pq == 0),
 // stopping test off(A) <= 10*n*eps*|C|_F checked once per sweep, 30-sweep cap and stable
 // descending sort (gram_qr.cpp:60-121).  The reference sweeps cyclic-by-row, one rotation at a
-// time; here the n/2 disjoint rotations J = J_1 ... J_{n/2} of a round-robin round are applied together
-// as one two-sided update A <- J^T A J.
+// time; here a sweep is a TWO-LEVEL round-robin: the indices form blocks of two, the blocks are paired
+// round-robin, and a block pair (I, J) = indices (a, b | c, d) is a GROUP that performs, back to back,
+//     set 0 (first block round of a sweep only):  (a, b), (c, d)      - the pairs inside the blocks
+//     set 1:  (a, c), (b, d)            set 2:  (a, d), (b, c)
+// so that every index pair is rotated once per sweep (np - 1 sets of np/2 disjoint rotations, the same count
+// as a plain round-robin), but A and U are read and written once per BLOCK round instead of once per set.
 //
 // One CTA, everything in shared memory:
 //   * A is kept as its packed upper triangle (a(i, j), i <= j, at j (j + 1) / 2 + i): 66 KB at 128 columns,
-//     which leaves room for the full U (132 KB) beside it - no global-memory U, no second pass.
-//   * A round = (1) one THREAD per pair derives (c, s) and writes the exact 2 x 2 result of its own diagonal
-//     block (gram_qr.cpp:84-87); (2) after a barrier one thread per unordered PAIR OF PAIRS (P, Q) updates the
-//     2 x 2 block A[P, Q] <- J_P^T (A[P, Q] J_Q) - four loads, 16 flops, four stores, each entry of the
-//     triangle touched once - while the warps rotate the columns of U; (3) barrier.
-//   The former column-phase / row-phase formulation over a full square A touched every entry twice with
-//   ~8 integer instructions per FMA and was ISSUE bound: 23.6 M warp instructions, 10 300 clk per round at
-//   n = 128 (ncu, round 2); this one issues about a quarter of that.
+//     which leaves room for the full U (132 KB) beside it.
+//   * A block round = (1) one THREAD per group loads its 4 x 4 diagonal block, derives the two or three sets of
+//     rotations from it (the two rotations of a set are independent chains the compiler interleaves) and
+//     writes the block back; (2) after a barrier one thread per unordered PAIR OF GROUPS (G, H) updates the
+//     4 x 4 block A[G, H] <- J_G^T A[G, H] J_H (16 loads, 128-192 flops, 16 stores; every entry of the triangle
+//     touched once) while a warp per group rotates four columns of U; (3) barrier.
+//   History (ncu, n = 128): column phase / row phase over a full square A with U in global memory: 23.6 M
+//   warp instructions, 7.9 ms, issue bound; one thread per 2 x 2 block pair, one set per round: 10.6 M, 3.1 ms,
+//   shared-memory pipe 84 % busy (U alone 40 % of the wavefronts) - hence the grouping.
 // Returns false when the sweep cap is hit.  On return lam[j] = eigenvalue at index j, perm[j] = source
 // index of output j, and column perm[j] of U the eigenvector.
 // ------------------------------------------------------------------------------------------------
-// The rotation scalars are a serial chain of two divisions, a square root and a reciprocal square root
-// per round; the IEEE software sequences for those cost ~3000 clk per round.  MUFU seed + two Newton steps
-// each (<= 1-2 ulp) take a tenth of that; the eigen-decomposition is compared through its invariants,
-// never bitwise.
+// The rotation scalars are a serial chain of two divisions, a square root and a reciprocal square root;
+// the IEEE software sequences for those cost ~3000 clk.  MUFU seed + two Newton steps each (<= 1-2 ulp)
+// take a tenth of that; the eigen-decomposition is compared through its invariants, never bitwise
+// (DESIGN.md, section 2).
 __device__ __forceinline__ double fast_rcp(double x) {
   double z;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(z) : "d"(x));
@@ -235,14 +237,79 @@ __device__ __forceinline__ double fast_rsqrt(double x) {  // x in [1, 1e200]
   return y;
 }
 
+// Rotation annihilating a_pq (gram_qr.cpp:74-83), branch-free: a_pq == 0 gives the identity (t = 0).
+__device__ __forceinline__ void jacobi_params(double app, double aqq, double apq, double& cs, double& sn, double& tt) {
+  const bool rot = apq != 0.0;
+  const double theta = (aqq - app) * fast_rcp(2.0 * (rot ? apq : 1.0));
+  const double ath = fabs(theta);
+  const double r2 = fma(theta, theta, 1.0);
+  const double y2 = fast_rsqrt(r2);
+  double sq = r2 * y2;
+  sq = fma(fma(-sq, sq, r2), 0.5 * y2, sq);  // sqrt(1 + theta^2), residual-corrected
+  const double t_small = (theta >= 0.0 ? 1.0 : -1.0) * fast_rcp(ath + sq);
+  // sqrt(1 + theta^2) == |theta| in working precision: t = 1 / (2 theta) (0 once that underflows)
+  const double t_big = ath < 1e300 ? fast_rcp(2.0 * (ath < 1e300 ? theta : 1.0)) : 0.0;
+  const double t = ath < 1e100 ? t_small : t_big;
+  const double c = fast_rsqrt(fma(t, t, 1.0));
+  tt = rot ? t : 0.0;
+  cs = rot ? c : 1.0;
+  sn = rot ? t * c : 0.0;
+}
+
+__device__ __forceinline__ void jrot(double& x, double& y, double c, double s) {
+  const double nx = c * x - s * y;
+  y = s * x + c * y;
+  x = nx;
+}
+
+// The rotation sets of a group on a 4-vector over its indices (a row of A[., G] / U[., G] or a column of A[G, .])
+__device__ __forceinline__ void apply_sets(double& v0, double& v1, double& v2, double& v3, const double* __restrict__ c,
+                                           const double* __restrict__ s, bool intra) {
+  if (intra) {
+    jrot(v0, v1, c[0], s[0]);
+    jrot(v2, v3, c[1], s[1]);
+  }
+  jrot(v0, v2, c[2], s[2]);
+  jrot(v1, v3, c[3], s[3]);
+  jrot(v0, v3, c[4], s[4]);
+  jrot(v1, v2, c[5], s[5]);
+}
+
+// Two disjoint rotations (X0, Y0), (X1, Y1) of the symmetric 4 x 4 diagonal block, two-sided, with the exact
+// 2 x 2 results (gram_qr.cpp:84-87)
+template <int X0, int Y0, int X1, int Y1>
+__device__ __forceinline__ void diag_set(double (&m)[4][4], double* c, double* s) {
+  double t0, t1;
+  jacobi_params(m[X0][X0], m[Y0][Y0], m[X0][Y0], c[0], s[0], t0);
+  jacobi_params(m[X1][X1], m[Y1][Y1], m[X1][Y1], c[1], s[1], t1);
+  const double p0 = m[X0][X0] - t0 * m[X0][Y0], q0 = m[Y0][Y0] + t0 * m[X0][Y0];
+  const double p1 = m[X1][X1] - t1 * m[X1][Y1], q1 = m[Y1][Y1] + t1 * m[X1][Y1];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    jrot(m[r][X0], m[r][Y0], c[0], s[0]);
+    jrot(m[r][X1], m[r][Y1], c[1], s[1]);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    jrot(m[X0][k], m[Y0][k], c[0], s[0]);
+    jrot(m[X1][k], m[Y1][k], c[1], s[1]);
+  }
+  m[X0][X0] = p0;
+  m[Y0][Y0] = q0;
+  m[X1][X1] = p1;
+  m[Y1][Y1] = q1;
+  if (t0 != 0.0) m[X0][Y0] = m[Y0][X0] = 0.0;
+  if (t1 != 0.0) m[X1][Y1] = m[Y1][X1] = 0.0;
+}
+
 struct JacobiScratch {
-  double* cs;      // np/2
-  double* sn;      // np/2
-  int2* pq;        // np/2: the (p, q), p < q, of pair t in this round
+  double* rc;      // G x 6: cosines of the group's rotations, set-major
+  double* rs;      // G x 6: sines
+  int2* gb;        // G: the block pair (I < J) of group slot t in this block round
   double* red;     // 32
   int* perm;       // n
   double* lam;     // n: the eigenvalues by index (diagonal of the converged A)
-  unsigned* blk;   // (np/2)(np/2 - 1)/2: the unordered pairs (tP < tQ) of pair slots, (tP << 16) | tQ
+  unsigned* blk;   // G (G - 1) / 2: the unordered pairs (tG < tH) of group slots, (tG << 16) | tH
 };
 
 __device__ __forceinline__ int tri_at(int i, int j) {  // packed upper triangle, either order
@@ -263,31 +330,32 @@ __device__ double block_sum(double v, double* red) {
 }
 
 // want_vectors = false skips U altogether (the sigma eigensolve of an SVQB pass only needs the eigenvalues).
-// `a`: packed upper triangle of order np = n rounded up to even, entries (i <= j < n) filled by the caller.
+// `a`: packed upper triangle of order np = n rounded up to a multiple of 4, entries (i <= j < n) filled by the
+// caller; `u`: n rows x np columns, pitch ldu.
 __device__ bool jacobi_eigh(double* a, double* u, int ldu, int n, const JacobiScratch& js, bool want_vectors = true) {
   const int tid = threadIdx.x, nt_ = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, nwarps = nt_ >> 5;
-  const int np = (n + 1) & ~1;
-  const int half = np / 2;
-  const int nblk = half * (half - 1) / 2;
+  const int np = (n + 3) & ~3;
+  const int nb2 = np / 2;      // index blocks of two
+  const int ng = nb2 / 2;      // groups (block pairs) per block round
+  const int nblk = ng * (ng - 1) / 2;
 
-  // the block list: the strict upper triangle of the half x half slot grid, folded into half/2 rows of
-  // half - 1 entries (row r of the triangle together with row half - 1 - r)
+  // the list of group pairs: the strict upper triangle of the ng x ng slot grid, folded into ng/2 rows of
+  // ng - 1 entries (row r of the triangle together with row ng - 1 - r)
   for (int k = tid; k < nblk; k += nt_) {
-    const int r = k / (half - 1), c = k % (half - 1);
-    int tp, tq;
-    if (c < half - 1 - r) {
-      tp = r;
-      tq = r + 1 + c;
+    const int r = k / (ng - 1), c = k % (ng - 1);
+    int tg, th;
+    if (c < ng - 1 - r) {
+      tg = r;
+      th = r + 1 + c;
     } else {
-      tp = half - 1 - r;
-      tq = tp + 1 + (c - (half - 1 - r));
+      tg = ng - 1 - r;
+      th = tg + 1 + (c - (ng - 1 - r));
     }
-    js.blk[k] = (static_cast<unsigned>(tp) << 16) | static_cast<unsigned>(tq);
+    js.blk[k] = (static_cast<unsigned>(tg) << 16) | static_cast<unsigned>(th);
   }
-  if (np > n) {  // padding index n: zero row/column, never rotated (a_pq == 0 rule)
-    for (int i = tid; i < np; i += nt_) a[tri_at(i, n)] = 0.0;
-  }
+  // padding indices n .. np - 1: zero rows / columns, never rotated (a_pq == 0 rule)
+  for (int idx = ((n * (n + 1)) >> 1) + tid; idx < ((np * (np + 1)) >> 1); idx += nt_) a[idx] = 0.0;
   // |C|_F and identity U
   double fro = 0.0;
   for (int idx = tid; idx < n * n; idx += nt_) {
@@ -296,8 +364,12 @@ __device__ bool jacobi_eigh(double* a, double* u, int ldu, int n, const JacobiSc
       const double v = a[tri_at(i, j)];
       fro = fma(i == j ? v : 2.0 * v, v, fro);
     }
-    if (want_vectors) u[i + j * ldu] = i == j ? 1.0 : 0.0;
   }
+  if (want_vectors)
+    for (int idx = tid; idx < n * np; idx += nt_) {
+      const int i = idx % n, j = idx / n;
+      u[i + j * ldu] = i == j ? 1.0 : 0.0;
+    }
   const double thr = 10.0 * static_cast<double>(n) * kEps * sqrt(block_sum(fro, js.red));
 
   auto offdiag = [&]() {
@@ -311,74 +383,100 @@ __device__ bool jacobi_eigh(double* a, double* u, int ldu, int n, const JacobiSc
 
   bool converged = offdiag() <= thr;
   for (int sweep = 0; sweep < kJacobiMaxSweeps && !converged; ++sweep) {
-    for (int step = 0; step < np - 1; ++step) {
-      // (1) rotation of pair slot t (round-robin: slot 0 keeps index np - 1)
-      if (tid < half) {
+    for (int step = 0; step < nb2 - 1; ++step) {
+      const bool intra = step == 0;
+      // (1) the group's rotations from its 4 x 4 diagonal block (round-robin over blocks: slot 0 keeps the last)
+      if (tid < ng) {
         const int t = tid;
         int x, y;
         if (t == 0) {
-          x = np - 1;
+          x = nb2 - 1;
           y = step;
         } else {
-          x = (step + t) % (np - 1);
-          y = (step - t + (np - 1)) % (np - 1);
+          x = (step + t) % (nb2 - 1);
+          y = (step - t + (nb2 - 1)) % (nb2 - 1);
         }
-        const int p = min(x, y), q = max(x, y);
-        const int ipp = ((p * (p + 1)) >> 1) + p, iqq = ((q * (q + 1)) >> 1) + q, ipq = ((q * (q + 1)) >> 1) + p;
-        const double apq = a[ipq];
-        double cs = 1.0, sn = 0.0;
-        if (apq != 0.0) {
-          const double app = a[ipp], aqq = a[iqq];
-          const double theta = (aqq - app) * fast_rcp(2.0 * apq);
-          const double ath = fabs(theta);
-          double tt;
-          if (ath < 1e100) {
-            const double r2 = fma(theta, theta, 1.0);
-            const double y2 = fast_rsqrt(r2);
-            double sq = r2 * y2;
-            sq = fma(fma(-sq, sq, r2), 0.5 * y2, sq);  // sqrt(1 + theta^2), residual-corrected
-            tt = (theta >= 0.0 ? 1.0 : -1.0) * fast_rcp(ath + sq);
-          } else {
-            tt = 0.5 / theta;  // sqrt(1 + theta^2) == |theta| in working precision (also theta = +-inf)
-          }
-          cs = fast_rsqrt(fma(tt, tt, 1.0));
-          sn = tt * cs;
-          a[ipp] = app - tt * apq;  // the exact 2 x 2 results (gram_qr.cpp:84-87)
-          a[iqq] = aqq + tt * apq;
-          a[ipq] = 0.0;
+        const int bi = min(x, y), bj = max(x, y);
+        const int g[4] = {2 * bi, 2 * bi + 1, 2 * bj, 2 * bj + 1};  // ascending
+        double m[4][4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int r = 0; r <= c; ++r) m[r][c] = m[c][r] = a[((g[c] * (g[c] + 1)) >> 1) + g[r]];
+        double c6[6], s6[6];
+        c6[0] = c6[1] = 1.0;
+        s6[0] = s6[1] = 0.0;
+        if (intra) diag_set<0, 1, 2, 3>(m, c6, s6);
+        diag_set<0, 2, 1, 3>(m, c6 + 2, s6 + 2);
+        diag_set<0, 3, 1, 2>(m, c6 + 4, s6 + 4);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int r = 0; r <= c; ++r) a[((g[c] * (g[c] + 1)) >> 1) + g[r]] = m[r][c];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          js.rc[t * 6 + k] = c6[k];
+          js.rs[t * 6 + k] = s6[k];
         }
-        js.cs[t] = cs;
-        js.sn[t] = sn;
-        js.pq[t] = make_int2(p, q);
+        js.gb[t] = make_int2(bi, bj);
       }
       __syncthreads();
-      // (2a) off-diagonal blocks: A[P, Q] <- J_P^T (A[P, Q] J_Q).  An unrotated pair has (c, s) = (1, 0): exact.
+      // (2a) off-diagonal blocks: A[G, H] <- J_G^T (A[G, H] J_H), sets in order on either side
       for (int k = tid; k < nblk; k += nt_) {
         const unsigned e = js.blk[k];
-        const int tp = e >> 16, tq = e & 0xffffu;
-        const int2 P = js.pq[tp], Q = js.pq[tq];
-        const double cp = js.cs[tp], sp = js.sn[tp], cq = js.cs[tq], sq = js.sn[tq];
-        const int i00 = tri_at(P.x, Q.x), i01 = tri_at(P.x, Q.y), i10 = tri_at(P.y, Q.x), i11 = tri_at(P.y, Q.y);
-        const double a00 = a[i00], a01 = a[i01], a10 = a[i10], a11 = a[i11];
-        const double b00 = cq * a00 - sq * a01, b01 = sq * a00 + cq * a01;  // columns: . J_Q
-        const double b10 = cq * a10 - sq * a11, b11 = sq * a10 + cq * a11;
-        a[i00] = cp * b00 - sp * b10;                                       // rows: J_P^T .
-        a[i10] = sp * b00 + cp * b10;
-        a[i01] = cp * b01 - sp * b11;
-        a[i11] = sp * b01 + cp * b11;
+        const int tg = e >> 16, th = e & 0xffffu;
+        const int2 gbk = js.gb[tg], hbk = js.gb[th];
+        const int gblk[2] = {gbk.x, gbk.y}, hblk[2] = {hbk.x, hbk.y};
+        int ix[4][4];
+        double m[4][4];
+#pragma unroll
+        for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+          for (int cb = 0; cb < 2; ++cb) {
+            // the four entries between index blocks gblk[rb] and hblk[cb] (distinct blocks: one is wholly above)
+            const int lo = 2 * min(gblk[rb], hblk[cb]), hi = 2 * max(gblk[rb], hblk[cb]);
+            const bool row_low = gblk[rb] < hblk[cb];
+            const int base0 = ((hi * (hi + 1)) >> 1) + lo, base1 = (((hi + 1) * (hi + 2)) >> 1) + lo;
+            // packed (lo + x, hi + y) = base_y + x; (row, col) = (lo + x, hi + y) when the row block is the lower
+            ix[2 * rb][2 * cb] = base0;
+            ix[2 * rb + 1][2 * cb + 1] = base1 + 1;
+            ix[2 * rb][2 * cb + 1] = row_low ? base1 : base0 + 1;
+            ix[2 * rb + 1][2 * cb] = row_low ? base0 + 1 : base1;
+          }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) m[r][c] = a[ix[r][c]];
+        {
+          const double* hc = js.rc + th * 6;
+          const double* hs = js.rs + th * 6;
+#pragma unroll
+          for (int r = 0; r < 4; ++r) apply_sets(m[r][0], m[r][1], m[r][2], m[r][3], hc, hs, intra);
+          const double* gc = js.rc + tg * 6;
+          const double* gs = js.rs + tg * 6;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) apply_sets(m[0][c], m[1][c], m[2][c], m[3][c], gc, gs, intra);
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) a[ix[r][c]] = m[r][c];
       }
-      // (2b) U <- U J: a warp per pair, lanes over the rows
+      // (2b) U <- U J: a warp per group, lanes over the rows
       if (want_vectors) {
-        for (int t = warp; t < half; t += nwarps) {
-          const double cs = js.cs[t], sn = js.sn[t];
-          if (sn == 0.0) continue;  // identity (this also keeps the padding index out of U)
-          const int2 P = js.pq[t];
-          double* up = u + P.x * ldu;
-          double* uq = u + P.y * ldu;
+        for (int t = warp; t < ng; t += nwarps) {
+          const int2 gbk = js.gb[t];
+          double* u0 = u + (2 * gbk.x) * ldu;
+          double* u2 = u + (2 * gbk.y) * ldu;
+          const double* gc = js.rc + t * 6;
+          const double* gs = js.rs + t * 6;
           for (int i = lane; i < n; i += 32) {
-            const double uip = up[i], uiq = uq[i];
-            up[i] = cs * uip - sn * uiq;
-            uq[i] = sn * uip + cs * uiq;
+            double v0 = u0[i], v1 = u0[i + ldu], v2 = u2[i], v3 = u2[i + ldu];
+            apply_sets(v0, v1, v2, v3, gc, gs, intra);
+            u0[i] = v0;
+            u0[i + ldu] = v1;
+            u2[i] = v2;
+            u2[i + ldu] = v3;
           }
         }
       }
@@ -412,28 +510,28 @@ struct SmallLayout {
 
 __host__ __device__ inline SmallLayout small_layout(int n) {
   SmallLayout L;
-  const int np = (n + 1) & ~1;
-  const int half = np / 2;
+  const int np = (n + 3) & ~3;
+  const int ng = np / 4;
   L.ldu = n + 1;
   L.a_off = 0;
-  size_t off = (static_cast<size_t>(np) * (np + 1) / 2 + 1) & ~static_cast<size_t>(1);
+  size_t off = static_cast<size_t>(np) * (np + 1) / 2;  // even: np is a multiple of 4
   L.u_off = off;
-  off += (static_cast<size_t>(n) * L.ldu + 1) & ~static_cast<size_t>(1);
+  off += (static_cast<size_t>(np) * L.ldu + 1) & ~static_cast<size_t>(1);
   L.misc_off = off;
-  // cs, sn, pq (half each), red (32), perm (n ints), lam (n), blk (half (half - 1) / 2 unsigned)
-  off += 3 * half + 32 + (n + 1) / 2 + 2 + np + (static_cast<size_t>(half) * (half - 1) / 2 + 1) / 2 + 2;
+  // rc, rs (6 ng each), gb (ng), red (32), perm (n ints), lam (n), blk (ng (ng - 1) / 2 unsigned)
+  off += 13 * ng + 32 + (n + 1) / 2 + 2 + np + (static_cast<size_t>(ng) * (ng - 1) / 2 + 1) / 2 + 2;
   L.total_doubles = off;
   return L;
 }
 
 __device__ JacobiScratch carve_scratch(double* sm, const SmallLayout& L, int n) {
-  const int np = (n + 1) & ~1;
-  const int half = np / 2;
+  const int np = (n + 3) & ~3;
+  const int ng = np / 4;
   JacobiScratch js;
   double* p = sm + L.misc_off;
-  js.cs = p; p += half;
-  js.sn = p; p += half;
-  js.pq = reinterpret_cast<int2*>(p); p += half;
+  js.rc = p; p += 6 * ng;
+  js.rs = p; p += 6 * ng;
+  js.gb = reinterpret_cast<int2*>(p); p += ng;
   js.red = p; p += 32;
   js.perm = reinterpret_cast<int*>(p); p += (n + 1) / 2 + 2;
   js.lam = p; p += np;

@@ -106,10 +106,13 @@ struct Fold {
   // One reflector step.  BC = slot of column c; PEEL: c is the last column of its slot (gc == G-1).
   // Written in phases so that every phase offers (live slots) independent FP64 chains: all dot
   // products, all update scalars, then the slot of column c+1, the lookahead reflector, the rest.
-  template <int BC, bool PEEL>
+  // GUARD: the triangle is only written when `store` (merge tree: a group without a partner folds zero rows
+  // beside the others because the shuffles are warp-wide; its triangle is being read by its own partner's
+  // owner at a lower slot, so it must not be written, not even with unchanged values).
+  template <int BC, bool PEEL, bool GUARD>
   static __device__ __forceinline__ void step(double (&w)[NS][P], double (&v)[P], Reflector& h,
                                               double* tri, int& rowoff, int g, int gc,
-                                              const NextChunk& nx) {
+                                              const NextChunk& nx, bool store) {
     constexpr int S1 = PEEL ? BC + 1 : BC;   // slot of column c+1
     constexpr int SLO = PEEL ? BC + 1 : BC;  // first slot that still has live columns
     constexpr bool HAS_NEXT = S1 < NS;
@@ -132,7 +135,7 @@ struct Fold {
     static_for<SLO, NS>([&](auto ss) {
       constexpr int s = decltype(ss)::value;
       acc[s] *= h.gamma;
-      if (s > BC || g > gc) rrow[s * G] = fma(-h.u0, acc[s], rrow[s * G]);
+      if ((!GUARD || store) && (s > BC || g > gc)) rrow[s * G] = fma(-h.u0, acc[s], rrow[s * G]);
     });
     Reflector hn;
     if constexpr (HAS_NEXT) {
@@ -156,7 +159,7 @@ struct Fold {
         if constexpr (!(HAS_NEXT && s == S1)) w[s][i] = fma(-v[i], acc[s], w[s][i]);
       });
     }
-    if (g == gc) tri[rowoff + c] = h.beta;
+    if ((!GUARD || store) && g == gc) tri[rowoff + c] = h.beta;
     if constexpr (PEEL && BC < NS - 1) refill<BC>(w, nx, g);
     if constexpr (HAS_NEXT) {
       if constexpr (G > 1) {
@@ -173,8 +176,9 @@ struct Fold {
 
   // Fold the group's P x n register panel into its triangle; on return the panel holds the rows
   // named by `nx` (or zeros).
+  template <bool GUARD = false>
   static __device__ __forceinline__ void run(double (&w)[NS][P], double* tri, int n, int g,
-                                             const NextChunk& nx) {
+                                             const NextChunk& nx, bool store = true) {
     double v[P];
     Reflector h;
     int rowoff = 0;
@@ -185,17 +189,17 @@ struct Fold {
       if constexpr (bc < NS - 1) {
         if constexpr (G > 1) {
 #pragma unroll 1
-          for (int gc = 0; gc < G - 1; ++gc) step<bc, false>(w, v, h, tri, rowoff, g, gc, nx);
+          for (int gc = 0; gc < G - 1; ++gc) step<bc, false, GUARD>(w, v, h, tri, rowoff, g, gc, nx, store);
         }
-        step<bc, true>(w, v, h, tri, rowoff, g, G - 1, nx);
+        step<bc, true, GUARD>(w, v, h, tri, rowoff, g, G - 1, nx, store);
       } else {
         const int cols_last = n - bc * G;  // 1..G live columns in the last slot
         if constexpr (G > 1) {
           const int lim = cols_last < G - 1 ? cols_last : G - 1;
 #pragma unroll 1
-          for (int gc = 0; gc < lim; ++gc) step<bc, false>(w, v, h, tri, rowoff, g, gc, nx);
+          for (int gc = 0; gc < lim; ++gc) step<bc, false, GUARD>(w, v, h, tri, rowoff, g, gc, nx, store);
         }
-        if (cols_last == G) step<bc, true>(w, v, h, tri, rowoff, g, G - 1, nx);
+        if (cols_last == G) step<bc, true, GUARD>(w, v, h, tri, rowoff, g, G - 1, nx, store);
         refill<bc>(w, nx, g);
       }
     });
@@ -281,7 +285,7 @@ __global__ void __launch_bounds__(FoldCfg<NS, G, P, TMAX>::T, 1) tsqr_fold_kerne
             const int row = base + i, col = s * G + g;
             w[s][i] = (has && row <= col && row < n) ? other[row_base(row, NPAD) + col] : 0.0;
           }
-        Fold<NS, G, P>::run(w, tri, n, g, nx);
+        Fold<NS, G, P>::template run<true>(w, tri, n, g, nx, has);
       }
     }
     active = half;

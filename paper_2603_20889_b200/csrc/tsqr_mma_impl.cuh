@@ -180,7 +180,9 @@ struct MmaFold {
         if (q == 0 && g < j) tbuf[g * 8 + j] = d;
       });
 
-      // diagonal tile back to the triangle (all q hold the same column; q == 0 writes)
+      // diagonal tile back to the triangle (all q hold the same column; q == 0 writes) - once every lane has read
+      // the last pivot of the sweep from it
+      __syncwarp();
       if (q == 0) {
 #pragma unroll
         for (int k = 0; k < 4; ++k)

@@ -21,8 +21,12 @@ for n in ns:
     m = (1 << log2e) // n
     m -= m % 2
     x = ctx.fill_gaussian(m, n, seed=1234)
-    fn = {"tsqr": ctx.tsqr_qless, "stage1": ctx.tsqr_stage1, "tsmttsm": ctx.tsmttsm,
-          "cholqr2": ctx.cholqr2, "svqb2": ctx.svqb2}[method]
+    if method in ("tsmRttsmR", "tsmmttsmm"):  # the second-pass kernels alone, factor = R of the matrix itself
+        r = ctx.cholqr2(x)
+        fn = (lambda xx: ctx.tsmRttsmR(xx, r)) if method == "tsmRttsmR" else (lambda xx: ctx.tsmmttsmm(xx, r))
+    else:
+        fn = {"tsqr": ctx.tsqr_qless, "stage1": ctx.tsqr_stage1, "tsmttsm": ctx.tsmttsm,
+              "cholqr2": ctx.cholqr2, "svqb2": ctx.svqb2}[method]
     for _ in range(2):
         fn(x)
     torch.cuda.synchronize()
