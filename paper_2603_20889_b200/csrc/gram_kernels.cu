@@ -521,11 +521,15 @@ static cudaError_t launch_gram_nb(const GramParams& prm, long long num_blocks, c
   return cudaGetLastError();
 }
 
-// 8 NB + R columns with R in 1..4 and 2 <= NB <= 4 (17..20, 25..28, 33..36): remainder on the FMA pipe
-// (the multiply pass only up to two remainder columns: its remainder entries reach the other column groups
-// through shuffles, which stop paying at three - measured)
+// 8 NB + R columns, 2 <= NB <= 4: the R remainder columns on the FMA pipe instead of a padded tile column,
+// wherever that measured faster than the padded (NB + 1)-tile kernel (profiles/probes/r02_remainder_ab.txt):
+// largest R per (operation, NB).  The multiply pass hands its remainder entries to the other column groups
+// through shuffles, the solve pass substitutes them with a padded DMMA from R = 2 on - both stop paying early.
 constexpr bool gram_remainder_variant(int n, int op) {
-  return n % 8 >= 1 && n % 8 <= (op == OP_MULTIPLY ? 2 : 4) && n / 8 >= 2 && n / 8 <= 4;
+  const int nb = n / 8, r = n % 8;
+  if (r == 0 || nb < 2 || nb > 4) return false;
+  const int max_r = op == OP_PLAIN ? (nb == 3 ? 3 : 4) : (op == OP_SOLVE ? (nb == 2 ? 4 : (nb == 3 ? 2 : 1)) : (nb == 4 ? 0 : 2));
+  return r <= max_r;
 }
 
 template <int NB, int OP>
