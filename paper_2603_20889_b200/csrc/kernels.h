@@ -146,7 +146,8 @@ cudaError_t launch_rinv_global(const double* r, int n, double* scratch_rowmajor,
 size_t small_scratch_doubles(int n);
 cudaError_t launch_eigh(const double* c, int n, double* values, double* vectors, double* scratch,
                         StatusWord* status, cudaStream_t stream);
-// scratch: at least n*(n+1) + 2*n doubles of device memory (U beyond 64 columns, the two diagonal scalings)
+// scratch: at least 2*n doubles of device memory (the two diagonal scalings; A and U live in shared memory).
+// want_sigma adds a second CTA that solves the unscaled Gram matrix for sigma beside the scaled solve.
 cudaError_t launch_svqb_pass(const double* c, int n, double* b, double* z, double* sigma,
                              long long* rank, int want_sigma, double* scratch, StatusWord* status,
                              cudaStream_t stream);

@@ -18,8 +18,6 @@ namespace sqb {
 namespace {
 
 constexpr int kSmallThreads = 256;
-// The Jacobi kernels scale their thread count with n: a round of the 64 x 64 problem rotates 2 x 2048
-// column / row entries of A and U, which 256 threads walk in 8 trips between CTA barriers.
 constexpr int kJacobiMaxThreads = 512;
 // a thread per pair of index groups (<= 496 at 128 columns) and a warp per group (<= 32), at 128 registers
 inline int jacobi_threads(int n) { return n <= 32 ? 256 : 512; }

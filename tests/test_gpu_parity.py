@@ -300,6 +300,38 @@ def test_cholesky_and_eigh(ctx, sq, oracle, n):
     assert np.linalg.norm(c @ vecs - vecs * vals) <= 50 * n * EPS * np.linalg.norm(c)
 
 
+@pytest.mark.parametrize("n", [3, 4, 6, 7, 33, 65, 66, 67, 95, 125, 126, 127])
+@pytest.mark.parametrize("kind", ["graded", "clustered", "rank1", "diagonal", "scaled"])
+def test_eigh_special_matrices(ctx, oracle, n, kind):
+    """The grouped Jacobi (index blocks of two, padding to a multiple of 4) on spectra the Gaussian Gram matrices
+    do not produce; eigenvalues against the reference's cyclic Jacobi (gram_qr.cpp:60-121), vectors through the
+    invariants."""
+    rng = np.random.default_rng(1000 * n + len(kind))
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    if kind == "graded":
+        lam = np.logspace(0, -12, n)
+    elif kind == "clustered":
+        lam = np.where(np.arange(n) % 2 == 0, 1.0, 1.0 + 1e-9) * (1.0 + np.arange(n) // 8)
+    elif kind == "rank1":
+        lam = np.zeros(n)
+        lam[0] = 3.0
+    elif kind == "diagonal":
+        lam, q = np.linspace(1.0, 2.0, n)[::-1].copy(), np.eye(n)
+    else:  # entries near the edge of the range (squares ~1e300, like the reference's own Frobenius norm allows)
+        lam = np.logspace(0, -6, n) * 1e150
+    c = (q * lam) @ q.T
+    c = np.asfortranarray(0.5 * (c + c.T))
+    vals, vecs = ctx.eigh_small(c)
+    vals_ref, _ = oracle.best.eigh_small(c)
+    scale = np.abs(lam).max()
+    assert np.all(np.diff(vals) <= 0.0)
+    assert np.linalg.norm(vals - vals_ref) <= 50 * n * EPS * scale
+    assert np.linalg.norm(vecs.T @ vecs - np.eye(n)) <= 50 * n * EPS
+    assert np.linalg.norm(c @ vecs - vecs * vals) <= 50 * n * EPS * scale
+    if kind == "diagonal":  # already converged: no rotation, U = I up to the sort
+        assert np.array_equal(vals, lam) and np.array_equal(np.abs(vecs), np.eye(n))
+
+
 @pytest.mark.parametrize("m,n", [(4000, 3), (20000, 8), (15000, 16), (12000, 32), (9000, 64)])
 def test_cholqr2_and_svqb2(ctx, oracle, m, n):
     x = gaussian(m, n, seed=m)
