@@ -204,6 +204,19 @@ if wide.exists():
     shutil.copy(wide, P / f"{tag}_wide.txt")
     out.append(f"\n## Wide column counts at m = 2^24 ({tag}_wide.txt; `tools/time_gram_wide.py`)\n\n```\n{wide.read_text().strip()}\n```")
 
+small = G / f"{tag}_small.txt"
+if small.exists():
+    shutil.copy(small, P / f"{tag}_small.txt")
+    out.append(f"\n## The n x n solves alone, one CTA each ({tag}_small.txt; `tools/time_small.py`, Gram matrix of a 65 536-row Gaussian)\n\n```\n{small.read_text().strip()}\n```")
+eg = G / f"{tag}_eigh_n128.source_summary.txt"
+if eg.exists():
+    shutil.copy(eg, P / f"{tag}_eigh_n128.source_summary.txt")
+    raw = G / f"{tag}_eigh_n128.raw.csv"
+    if raw.exists():
+        shutil.copy(raw, P / f"{tag}_eigh_n128.raw.csv")
+    head = "\n".join(eg.read_text().splitlines()[:24])
+    out.append(f"\n## `eigh_kernel` at 128 x 128 (grouped Jacobi; ncu source page summary, {tag}_eigh_n128.*)\n\n```\n{head}\n```")
+
 clk = G / f"{tag}_clocks.csv"
 if clk.exists():
     shutil.copy(clk, P / f"{tag}_clocks.csv")
@@ -236,6 +249,9 @@ if san.exists():
 rw = G / f"{tag}_race_wide.txt"
 if rw.exists():
     out.append(f"\nRe-run on the final fused-kernel geometry (32-row solve panels, 2-stage ring):\n\n```\n{rw.read_text().strip()}\n```")
+rem = P / "probes" / f"{tag}_remainder_ab.txt"
+if rem.exists():
+    out.append(f"\n## Remainder-column variants against the padded kernels (profiles/probes/{rem.name})\n\n```\n{rem.read_text().strip()}\n```")
 probe = P / "probes" / f"{tag}_tsqr_experiments.txt"
 if probe.exists():
     out.append(f"\n## Kernel experiments of this round that were measured and dropped (profiles/probes/{probe.name})\n\n```\n{probe.read_text().strip()}\n```")
