@@ -15,5 +15,5 @@ echo 'compute-sanitizer --tool racecheck python -m pytest tests/test_gpu_parity.
 timeout 900 compute-sanitizer --tool racecheck python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "300-256" 2>&1 | tail -2 >> gpurun_out/${TAG}_sanitizer.txt
 echo 'compute-sanitizer --tool memcheck python -m pytest tests/test_sharded_gpu.py tests/test_gpu_golden.py -m gpu -k "not multi_process"' >> gpurun_out/${TAG}_sanitizer.txt
 timeout 900 compute-sanitizer --tool memcheck python -m pytest tests/test_sharded_gpu.py tests/test_gpu_golden.py -m gpu -x -q -k "not multi_process" 2>&1 | tail -2 >> gpurun_out/${TAG}_sanitizer.txt
-echo 'compute-sanitizer --tool racecheck python -m pytest tests/test_gpu_parity.py -m gpu -k "eigh or svqb"   (block-parallel Jacobi: packed triangle + U in shared memory)' >> gpurun_out/${TAG}_sanitizer.txt
-timeout 900 compute-sanitizer --tool racecheck python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "eigh or svqb" 2>&1 | tail -2 >> gpurun_out/${TAG}_sanitizer.txt
+echo 'compute-sanitizer --tool racecheck python -m pytest tests/test_gpu_parity.py -m gpu -k "(eigh or svqb) and not special"   (grouped Jacobi: packed triangle + U in shared memory)' >> gpurun_out/${TAG}_sanitizer.txt
+timeout 1500 compute-sanitizer --tool racecheck python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "(eigh or svqb) and not special" 2>&1 | tail -2 >> gpurun_out/${TAG}_sanitizer.txt
