@@ -78,6 +78,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// 16-byte asynchronous copy global -> shared issued per lane (LDGSTS, L2 only), tracked by per-thread commit
+// groups.  A warp moves 512 bytes per instruction with per-lane addresses; cp.async.bulk takes uniform operands,
+// so "one bulk copy per column" compiles to an election loop of ~9 instructions per column.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int PENDING>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(PENDING) : "memory");
+}
+
 // ---------------------------------------------------------------------------------------
 // FP64 helpers
 // ---------------------------------------------------------------------------------------

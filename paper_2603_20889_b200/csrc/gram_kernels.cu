@@ -100,6 +100,19 @@ struct GramCfg {
   static constexpr size_t kSmemBytes =
       sizeof(double) * (static_cast<size_t>(kWarpDoubles) * NW + kFacDoubles);
   static constexpr int NPAIR = NB * (NB + 1) / 2;
+  // How a warp fills its stages.  cp.async.bulk takes uniform operands, so "one bulk copy per column" compiles
+  // to an election loop of ~9 instructions per column and panel (40-64 columns: as many issue slots as the
+  // panel's DMMAs, and with two warps per scheduler the tensor pipe idles whenever both are in it: 62 / 73 /
+  // 80 % DMMA pipe at 40 / 48 / 56 columns against 88 % at 64).  Per-lane 16-byte cp.async copies (LDGSTS,
+  // commit groups) move a panel in P * NCOL / 64 instructions: plain pass +14 / +17 / +28 % at 40 / 48 / 56
+  // columns, solve pass +9 % from 48 columns and +14 / +19 % at 17 / 33, multiply pass +8 % from 48.  The bulk
+  // form stays where it measured faster (profiles/probes/r02_lane_copies_ab.txt).
+#ifndef SQB_GRAM_LANE_COPIES
+#define SQB_GRAM_LANE_COPIES 1
+#endif
+  static constexpr bool kLaneCopies =
+      SQB_GRAM_LANE_COPIES != 0 &&
+      (OP == OP_PLAIN ? R == 0 : (NB >= 4 || R > 0));
   static_assert(P >= 8 && P % 8 == 0, "panel rows");
   static_assert(kSmemBytes * kCtas + 1024 * kCtas <= 227 * 1024, "shared memory budget");
   static_assert(R == 0 || OP == OP_PLAIN || OP == OP_MULTIPLY || kBlockedSolve, "remainder variants");
@@ -218,24 +231,34 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
   uint32_t phase_bits = 0;   // bit s = parity to wait for on stage s
   uint32_t async_bits = 0;   // bit s = stage s was filled by the async engine
 
+  constexpr bool kLaneCopies = Cfg::kLaneCopies;
   auto issue = [&](long long pnl, int s) {
-    const bool a = issue_panel<P, PP, SWZ>(prm.x, n, begin + pnl * P, end, aligned,
-                                      my + s * Cfg::kStageDoubles, bars + s, lane);
-    async_bits = a ? (async_bits | (1u << s)) : (async_bits & ~(1u << s));
+    if constexpr (kLaneCopies) {
+      if (pnl < npanels)
+        issue_panel_lanes<P, PP, SWZ>(prm.x, n, begin + pnl * P, end, aligned, my + s * Cfg::kStageDoubles, lane);
+      cp_async_commit();  // one group per slot, empty past the last panel: the wait below counts groups
+    } else {
+      if (pnl >= npanels) return;
+      const bool a = issue_panel<P, PP, SWZ>(prm.x, n, begin + pnl * P, end, aligned,
+                                        my + s * Cfg::kStageDoubles, bars + s, lane);
+      async_bits = a ? (async_bits | (1u << s)) : (async_bits & ~(1u << s));
+    }
   };
 
   // prologue: fill all stages
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
-    const long long pnl = warp + static_cast<long long>(s) * NW;
-    if (pnl < npanels) issue(pnl, s);
+    issue(warp + static_cast<long long>(s) * NW, s);
   }
 
   long long it = 0;
   for (long long pnl = warp; pnl < npanels; pnl += NW, ++it) {
     const int s = static_cast<int>(it % NS);
     const double* stage = my + s * Cfg::kStageDoubles;
-    if (async_bits & (1u << s)) {
+    if constexpr (kLaneCopies) {
+      cp_async_wait<NS - 1>();
+      __syncwarp();
+    } else if (async_bits & (1u << s)) {
       mbar_wait(bars + s, (phase_bits >> s) & 1u);
       phase_bits ^= 1u << s;
     }
@@ -273,7 +296,7 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
         }
       }
       __syncwarp();
-      if (pnl + static_cast<long long>(NS) * NW < npanels) issue(pnl + static_cast<long long>(NS) * NW, s);
+      issue(pnl + static_cast<long long>(NS) * NW, s);
     } else if (Cfg::kBlockedSolve) {
       // Y = X R^-1 by 8-column blocks, 8 rows at a time, transposed so that the result lands in the
       // Gram fragment layout: Y_b^T = Rbb^-T (X_b^T - sum_{a<b} R_ab^T Y_a^T).  Finished blocks are
@@ -399,7 +422,7 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
         }
       }
       __syncwarp();
-      if (pnl + static_cast<long long>(NS) * NW < npanels) issue(pnl + static_cast<long long>(NS) * NW, s);
+      issue(pnl + static_cast<long long>(NS) * NW, s);
     } else {  // OP_MULTIPLY
       const int kchunks = (n + 3) / 4;
       // MU row groups advance together: NT * MU independent DMMA chains of length kchunks, and every
@@ -453,11 +476,12 @@ __global__ void __launch_bounds__(GramCfg<NB, OP, R>::NW * kWarp, GramCfg<NB, OP
         }
       }
       __syncwarp();
-      if (pnl + static_cast<long long>(NS) * NW < npanels) issue(pnl + static_cast<long long>(NS) * NW, s);
+      issue(pnl + static_cast<long long>(NS) * NW, s);
     }
   }
 
   // ---- CTA reduction in fixed warp order, then the block's upper-triangle partial -------------
+  if constexpr (kLaneCopies) cp_async_wait<0>();
   __syncthreads();  // all stages drained: the stage area becomes the CTA sum
   for (int i = threadIdx.x; i < Cfg::kSumDoubles; i += NW * kWarp) csum[i] = 0.0;
   for (int wi = 0; wi < NW; ++wi) {

@@ -338,13 +338,13 @@ cudaError_t launch_cfg(const TsqrParams& prm, long long num_blocks, cudaStream_t
     case 10: return EXPR(10, 1, 10, 256);     \
     case 11: return EXPR(11, 1, 8, 256);      \
     case 12: return EXPR(12, 1, 8, 256);      \
-    case 13: return EXPR(13, 1, 6, 256);      \
+    case 13: return EXPR(13, 1, 8, 256);      \
     case 14: return EXPR(14, 1, 6, 256);      \
     default: break;                           \
   }                                           \
   if (n <= 16) return EXPR(8, 2, 12, 256);    \
   if (n <= 18) return EXPR(9, 2, 10, 256);    \
-  if (n <= 20) return EXPR(10, 2, 8, 256);    \
+  if (n <= 20) return EXPR(10, 2, 10, 256);   \
   if (n <= 24) return EXPR(6, 4, 14, 256);    \
   if (n <= 28) return EXPR(7, 4, 12, 256);    \
   if (n <= 32) return EXPR(8, 4, 12, 256);    \

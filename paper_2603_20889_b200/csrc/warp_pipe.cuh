@@ -69,6 +69,30 @@ __device__ __forceinline__ bool issue_panel(const MatView& x, int n, long long r
   return false;
 }
 
+// The same fill with per-lane 16-byte asynchronous copies (commit groups instead of an mbarrier): lane l takes
+// the 16-byte chunks l, l + 32, ... of the panel, P / 2 chunks per column.  The caller commits one group per
+// call (also when nothing was issued) and waits with cp_async_wait<NS - 1>() + __syncwarp().
+template <int P, int PP, bool SWZ = false>
+__device__ __forceinline__ void issue_panel_lanes(const MatView& x, int n, long long r0, long long end,
+                                                  bool aligned, double* stage, int lane) {
+  const long long left = end - r0;
+  if (aligned && left >= P) {
+    constexpr int CH = P / 2;
+    const int total = n * CH;
+    for (int c = lane; c < total; c += kWarp) {
+      const int j = c / CH, r = c - j * CH;
+      cp_async16(stage + stage_col_offset<PP, SWZ>(j) + 2 * r, x.col(j) + r0 + 2 * r);
+    }
+    return;
+  }
+  const int live = static_cast<int>(left < P ? left : P);
+  for (int j = 0; j < n; ++j) {
+    const double* src = x.col(j) + r0;
+    for (int r = lane; r < P; r += kWarp) stage[stage_col_offset<PP, SWZ>(j) + r] = r < live ? __ldg(src + r) : 0.0;
+  }
+  __syncwarp();
+}
+
 // Running triangle of the TSQR kernels: packed ROW-major upper triangle of order npad; row c holds
 // (c, c..npad-1).  row_base(c) + j addresses entry (c, j); consecutive rows differ by npad - c - 1,
 // so a factorisation walks it with one running offset and no index multiplications.
