@@ -1,7 +1,8 @@
 """Wide Gram (config 5) timing: python tools/time_gram_wide.py [LOG2_M]  -> ms, GB/s, executed DMMA TFLOP/s"""
 import sys
 from pathlib import Path
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import os  # noqa: E402
+sys.path.insert(0, os.environ.get("SQB_PKG_ROOT", str(Path(__file__).resolve().parents[1])))  # A/B: an older build
 import torch  # noqa: E402
 import paper_2603_20889_b200 as sq  # noqa: E402
 
