@@ -28,6 +28,7 @@ import os
 import socket
 import subprocess
 import sys
+import tempfile
 import threading
 import time
 from pathlib import Path
@@ -211,11 +212,17 @@ class Rig:
         self.dev = torch.device(f"cuda:{self.local}")
         self.dist = None
         self.transport = None
+        self.nccl_log = None
         self.ctx = sq.Context(self.local)
         self.ctx.use_torch_stream()
         if self.world > 1:
             import torch.distributed as dist
-            os.environ.setdefault("NCCL_DEBUG", "INFO" if self.rank == 0 else "WARN")  # communicator log stays on
+            # the communicator log stays on, but NCCL writes INFO lines to stdout by default, where the one
+            # JSON line belongs: send them to a file and replay it on stderr when the run is over
+            os.environ.setdefault("NCCL_DEBUG", "INFO" if self.rank == 0 else "WARN")
+            if "NCCL_DEBUG_FILE" not in os.environ:
+                self.nccl_log = os.path.join(tempfile.gettempdir(), f"sqb_nccl_{os.getpid()}.log")
+                os.environ["NCCL_DEBUG_FILE"] = self.nccl_log
             dist.init_process_group("nccl", device_id=self.dev)
             self.dist = dist
             self.transport = sharding.attach(self.ctx, dist)  # the library's own NCCL communicator
@@ -256,6 +263,10 @@ class Rig:
     def close(self):
         if self.dist is not None:
             self.dist.destroy_process_group()
+        if self.nccl_log and os.path.exists(self.nccl_log):
+            with open(self.nccl_log, errors="replace") as f:
+                sys.stderr.write(f.read())
+            os.unlink(self.nccl_log)
 
 
 def traffic_per_launch(method, n, m):
