@@ -208,6 +208,11 @@ class Rig:
         self.rank = int(os.environ.get("RANK", "0"))
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        # flow check on a one-GPU box (--share-gpu): every rank on cuda:0, gloo process group, the library's
+        # exchange hook instead of NCCL (which refuses two ranks on one device) - never a scaling number
+        share = os.environ.get("SQB_BENCH_SHARE_GPU") == "1"
+        if share:
+            self.local = 0
         torch.cuda.set_device(self.local)
         self.dev = torch.device(f"cuda:{self.local}")
         self.dist = None
@@ -223,9 +228,13 @@ class Rig:
             if "NCCL_DEBUG_FILE" not in os.environ:
                 self.nccl_log = os.path.join(tempfile.gettempdir(), f"sqb_nccl_{os.getpid()}.log")
                 os.environ["NCCL_DEBUG_FILE"] = self.nccl_log
-            dist.init_process_group("nccl", device_id=self.dev)
+            if share:
+                dist.init_process_group("gloo")
+                self.transport = sharding.attach(self.ctx, dist) + " over gloo, ranks share cuda:0 (flow check only)"
+            else:
+                dist.init_process_group("nccl", device_id=self.dev)
+                self.transport = sharding.attach(self.ctx, dist)  # the library's own NCCL communicator
             self.dist = dist
-            self.transport = sharding.attach(self.ctx, dist)  # the library's own NCCL communicator
 
     def sync_all(self):
         self.torch.cuda.synchronize()
@@ -560,7 +569,11 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep-reps", type=int, default=50)
     ap.add_argument("--cpu-rows", type=int, default=0)
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="flow check on a one-GPU box: all ranks on cuda:0 over gloo (not a scaling number)")
     args = ap.parse_args()
+    if args.share_gpu:
+        os.environ["SQB_BENCH_SHARE_GPU"] = "1"
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -569,7 +582,7 @@ def main():
         # no launcher around us: start one process per GPU ourselves
         import torch
         have = torch.cuda.device_count()
-        if have < args.gpus:
+        if have < args.gpus and not args.share_gpu:
             raise SystemExit(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible")
         return sys.exit(subprocess.call(spawn_command(args.gpus, sys.argv[1:], free_port())))
 

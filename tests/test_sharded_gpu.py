@@ -116,3 +116,24 @@ def test_sharded_drivers_multi_process_one_gpu(tmp_path, oracle, world, m, n):
     xs_ref, res_ref = best.solve_lstsq(a, rhs, "tsqr")
     assert np.allclose(o["xs"], xs_ref, rtol=1e-9, atol=1e-12)
     assert abs(float(o["res"][0]) - res_ref) <= 1e-10 * max(res_ref, 1.0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("extra", [["--m", "2097152", "--no-cpu"], ["--config", "c4", "--c4-rows", "4000000"]])
+def test_bench_multi_rank_flow_on_one_gpu(extra):
+    """`bench.py --gpus 2` end to end - it starts its own ranks, every rank runs the sharded drivers, rank 0
+    prints exactly one JSON line with n_gpus = 2 - with both ranks on cuda:0 over gloo (`--share-gpu`: NCCL
+    refuses two ranks on one device).  A flow check of the launcher path, not a scaling number."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    out = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--share-gpu", "--steps", "3",
+                          "--warmup", "3", "--no-sweep"] + extra, capture_output=True, text=True, cwd=root, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] > 0
+    assert "flow check" in d["config"]["transport"]
