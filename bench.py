@@ -52,8 +52,16 @@ def measured_peaks():
 
 def spawn_command(n_gpus, argv, port):
     """The command `--gpus N` re-executes when no torchrun environment is present."""
+    # the launcher's own argument parser prefix-matches options placed after the script name (`--m` and `--n` are
+    # ambiguous prefixes of its `--master-addr`, `--nnodes`, ...): only the contract's three flags go on the
+    # command line, the full argument list travels in SQB_BENCH_ARGV (see main)
+    os.environ["SQB_BENCH_ARGV"] = json.dumps(list(argv))
     return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n_gpus}",
-            "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py")] + list(argv)
+            "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py"), "--gpus", str(n_gpus)]
+
+
+def rows_label(m):
+    return f"2^{m.bit_length() - 1}" if m > 0 and m & (m - 1) == 0 else str(m)
 
 
 def free_port():
@@ -391,7 +399,7 @@ def run_headline(rig, args):
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.method} m=2^27 n={n} Gaussian (BASELINE configs[1], headline point of the "
+        "config": {"workload": f"{args.method} m={rows_label(m)} n={n} Gaussian (BASELINE configs[1], headline point of the "
                                f"column sweep); value = SUSTAINED (K steps after 300 ms of untimed back-to-back "
                                f"steps, board on its power cap), burst = the same K steps on a settled board",
                    "m_per_gpu": m, "n": n, "method": args.method,
@@ -571,7 +579,8 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=0)
     ap.add_argument("--share-gpu", action="store_true",
                     help="flow check on a one-GPU box: all ranks on cuda:0 over gloo (not a scaling number)")
-    args = ap.parse_args()
+    forwarded = os.environ.get("SQB_BENCH_ARGV") if "WORLD_SIZE" in os.environ else None
+    args = ap.parse_args(json.loads(forwarded)) if forwarded else ap.parse_args()
     if args.share_gpu:
         os.environ["SQB_BENCH_SHARE_GPU"] = "1"
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup

@@ -101,7 +101,34 @@ def test_bench_spawn_command():
     """bench.py --gpus N (no torchrun around it) re-executes itself under torch.distributed.run."""
     sys.path.insert(0, str(ROOT))
     import bench
-    cmd = bench.spawn_command(4, ["--gpus", "4", "--steps", "5"], port=29999)
+    import json
+    import os
+    argv = ["--gpus", "4", "--steps", "5", "--m", "1024", "--n", "8"]
+    cmd = bench.spawn_command(4, argv, port=29999)
     assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
     assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd and "--master-port=29999" in cmd
-    assert cmd[-4:] == ["--gpus", "4", "--steps", "5"] and cmd[-5].endswith("bench.py")
+    # nothing the launcher's parser could prefix-match (--m, --n) follows the script name; the rest is forwarded
+    assert cmd[-2:] == ["--gpus", "4"] and cmd[-3].endswith("bench.py")
+    assert json.loads(os.environ.pop("SQB_BENCH_ARGV")) == argv
+
+
+def test_launcher_parser_accepts_the_spawn_command():
+    """torch.distributed.run must parse the command line bench.py builds (its parser rejects `--m` / `--n`
+    after the script name as ambiguous prefixes of its own options)."""
+    import os
+    sys.path.insert(0, str(ROOT))
+    import bench
+    from torch.distributed.run import get_args_parser
+    cmd = bench.spawn_command(2, ["--gpus", "2", "--m", "4096", "--n", "8", "--no-sweep"], port=29998)
+    os.environ.pop("SQB_BENCH_ARGV")
+    ns = get_args_parser().parse_args(cmd[3:])
+    assert ns.training_script.endswith("bench.py") and ns.training_script_args == ["--gpus", "2"]
+    # the driver's own launch line parses as well
+    ns = get_args_parser().parse_args(["--nnodes=1", "--nproc-per-node", "8", "--master-addr", "127.0.0.1",
+                                       "--master-port", "29500", "bench.py", "--gpus", "8", "--steps", "20",
+                                       "--warmup", "3"])
+    assert ns.training_script_args == ["--gpus", "8", "--steps", "20", "--warmup", "3"]
+    ns = get_args_parser().parse_args(["--nnodes=1", "--nproc-per-node", "8", "--master-addr", "127.0.0.1",
+                                       "--master-port", "29500", "bench.py", "--impl", "reference", "--gpus", "8",
+                                       "--steps", "20", "--warmup", "3"])
+    assert ns.training_script_args[:2] == ["--impl", "reference"]

@@ -244,6 +244,9 @@ if alln.exists():
         r = tab[nn]
         out.append(f"| {nn} | {r.get('tsqr', 0):.0f} | {r.get('cholqr2', 0):.0f} | {r.get('svqb2', 0):.0f} | {r.get('tsmttsm', 0):.0f} |")
 san = G / f"{tag}_sanitizer.txt"
+kept = P / f"{tag}_sanitizer.txt"  # the pool's compute-sanitizer was closed late in round 2: keep the last real pass
+if san.exists() and "is closed on this pool" in san.read_text() and kept.exists():
+    san = kept
 if san.exists():
     out.append(f"\n## compute-sanitizer (memcheck on the GPU parity suite, racecheck on the Gram / TSQR parity tests)\n\n```\n{san.read_text().strip()}\n```")
 rw = G / f"{tag}_race_wide.txt"
