@@ -339,7 +339,7 @@ def run_headline(rig, args):
         def rest_of_step():  # stage 2: one block over the k stacked triangles, sign-normalised
             ctx._check(lib.sqb_tsqr_qless_dev(ctx.handle, vp(y), I64(k * n), I64(n), I64(k * n), I64(1),
                                               I64(k * n), vp(r_out)), "stage2")
-        kname = ("tsqr_thread_kernel" if n <= 4 else "tsqr_fold_kernel" if n <= 28 else "tsqr_mma_kernel") + \
+        kname = ("tsqr_thread_kernel" if n <= 2 else "tsqr_fold_kernel" if n <= 28 else "tsqr_mma_kernel") + \
                 " (stage 1: one launch streams X once)"
     else:
         c_out = ctx.empty_matrix(n, n)

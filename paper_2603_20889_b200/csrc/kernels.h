@@ -27,8 +27,9 @@ cudaError_t launch_tsqr_thread(const TsqrParams& prm, long long num_blocks, cuda
 int tsqr_thread_chunk_rows(int n);
 int tsqr_thread_warps(int n);
 
-// ---- tsqr_fold_kernels.cu (5 <= n <= 64: lookahead lane-group kernel with retire loads) -------
-constexpr int kFoldTsqrMinN = 5;
+// ---- tsqr_fold_kernels.cu (3 <= n <= 64: lookahead lane-group kernel with retire loads) -------
+constexpr int kFoldTsqrMinN = 3;   // smallest column count the family is instantiated for
+constexpr int kFoldTsqrAutoMinN = 3;  // ... and the smallest one the selection table gives it
 cudaError_t launch_tsqr_fold(const TsqrParams& prm, long long num_blocks, cudaStream_t stream);
 int tsqr_fold_chunk_rows(int n);
 int tsqr_fold_warps(int n);
@@ -40,7 +41,7 @@ int tsqr_mma_panel_rows(int n);
 int tsqr_mma_warps(int n);
 
 // Kernel selection by column count (measured on B200, profiles/README.md): register-resident thread
-// kernel up to 4 columns, lookahead fold kernel for 5..28, DMMA blocked kernel for 29..64.  A
+// kernel up to 2 columns, lookahead fold kernel for 3..28, DMMA blocked kernel for 29..64.  A
 // context may force one family where the column count allows it (sqb_set_tsqr_kernel: A/B timing
 // and the kernel-family parity test); a family that cannot run this n falls back to the table.
 enum TsqrKind { kTsqrAuto = -1, kTsqrThread = 0, kTsqrFold = 1, kTsqrMma = 2 };
@@ -48,7 +49,7 @@ inline int tsqr_kernel_kind(int n, int forced) {
   if (forced == kTsqrThread && n <= kThreadTsqrMaxN) return kTsqrThread;
   if (forced == kTsqrFold && n >= kFoldTsqrMinN) return kTsqrFold;
   if (forced == kTsqrMma && n >= kMmaTsqrMinN) return kTsqrMma;
-  if (n < kFoldTsqrMinN) return kTsqrThread;
+  if (n < kFoldTsqrAutoMinN) return kTsqrThread;
   if (n <= 28) return kTsqrFold;
   return kTsqrMma;
 }

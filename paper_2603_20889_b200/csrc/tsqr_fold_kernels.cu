@@ -1,4 +1,4 @@
-// Lookahead lane-group Q-less Householder TSQR, 5 <= n <= 64  ("fold" kernels).
+// Lookahead lane-group Q-less Householder TSQR, 3 <= n <= 64  ("fold" kernels).
 //
 // Reference semantics: block_qless_qr_core / factor_trapezoidal / make_reflector
 // (reference src/tsqr.cpp:51-158): fold row panels into a running upper triangle with Householder
@@ -325,11 +325,15 @@ cudaError_t launch_cfg(const TsqrParams& prm, long long num_blocks, cudaStream_t
 
 // column count -> (slots per lane, lanes per group, rows per step, max threads per CTA); measured
 // on B200 (gpurun_out/fold_select.txt, profiles/README.md): thread-private leaves up to 14 columns
-// (5..8 columns: taller steps than the register-triangle kernel, 5-9 % faster under the power cap),
+// (5..8 columns: taller steps than the register-triangle kernel, 5-9 % faster under the power cap;
+// 3 and 4 columns: 2-4 % slower than it on a settled board, 7-11 % faster on the power cap, which is what a
+// long run sees - profiles/probes/r02_fold_n3_n4_sustained.txt),
 // lane pairs up to 20, lane quads up to 28; above that the DMMA kernel (tsqr_mma_kernels.cu) wins
 // and the last three rows only serve a forced kernel family (sqb_set_tsqr_kernel)
 #define SQB_FOLD_SWITCH(EXPR)                 \
   switch (n) {                                \
+    case 3: return EXPR(3, 1, 16, 256);       \
+    case 4: return EXPR(4, 1, 20, 256);       \
     case 5: return EXPR(5, 1, 16, 256);       \
     case 6: return EXPR(6, 1, 16, 256);       \
     case 7: return EXPR(7, 1, 12, 256);       \

@@ -551,7 +551,7 @@ def test_every_tsqr_kernel_family(kind, sq, oracle):
     c2 = sq.Context(0)
     c2.set_tsqr_kernel(kind)
     try:
-        for m, n in [(9000, 5), (9001, 11), (20000, 16), (30011, 17), (7000, 24), (40000, 29), (40002, 32),
+        for m, n in [(12345, 3), (3, 3), (9002, 4), (801, 4), (9000, 5), (9001, 11), (20000, 16), (30011, 17), (7000, 24), (40000, 29), (40002, 32),
                      (6000, 33), (9000, 47), (5000, 64), (70000, 64)]:
             x = gaussian(m, n, seed=n)
             x[:, n // 2] = 1.0

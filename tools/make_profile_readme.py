@@ -147,7 +147,7 @@ if raws:
         kern[k] = {"bytes": b, "m": 2 ** round(math.log2(b / (8.0 * nn)))}
     tj = {"_source": f"profiles/{tag}_*.raw.csv (ncu --set full): dram__bytes_read.sum + dram__bytes_write.sum per launch of the "
                      "streaming kernel, with the row count of the capture; bench.py scales to its own m", "kernels": kern}
-    for nn, key in ((4, "tsqr_thread_n4"), (8, "tsqr_fold_n8"), (12, "tsqr_fold_n12"), (16, "tsqr_fold_n16"), (24, "tsqr_fold_n24"),
+    for nn, key in ((2, "tsqr_thread_n2"), (4, "tsqr_fold_n4"), (8, "tsqr_fold_n8"), (12, "tsqr_fold_n12"), (16, "tsqr_fold_n16"), (24, "tsqr_fold_n24"),
                     (32, "tsqr_mma_n32"), (64, "tsqr_mma_n64")):
         if key in kern:
             tj[f"tsqr_n{nn}"] = kern[key]

@@ -21,7 +21,8 @@ prof() { # name kernel-regex method n log2m : full capture, kept as the raw-metr
   rm -f $O/${TAG}_$1.ncu-rep
 }
 prof tsqr_fold_n8 tsqr_fold stage1 8 27
-prof tsqr_thread_n4 tsqr_thread stage1 4 27
+prof tsqr_thread_n2 tsqr_thread stage1 2 28
+prof tsqr_fold_n4 tsqr_fold stage1 4 27
 prof tsqr_fold_n12 tsqr_fold stage1 12 27
 prof tsqr_fold_n16 tsqr_fold stage1 16 27
 prof tsqr_fold_n24 tsqr_fold stage1 24 26
