@@ -4,7 +4,8 @@ import sys
 import time
 from pathlib import Path
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import os
+sys.path.insert(0, os.environ.get("SQB_PKG_ROOT", str(Path(__file__).resolve().parents[1])))  # A/B: another build
 import torch  # noqa: E402
 import paper_2603_20889_b200 as sq  # noqa: E402
 
