@@ -63,6 +63,13 @@ __device__ __forceinline__ void ld2_pred(double& a, double& b, const double* p, 
       : "l"(p), "r"(pred));
 }
 
+// the same without predicate and zero fill: full chunks of a thread-private leaf (G == 1: every slot is a live
+// column).  The two zero moves per load pair of the predicated form are ALU-pipe instructions, which share the
+// FP64 dispatch slot - on the power cap the 8-column kernel is dispatch-bound
+__device__ __forceinline__ void ld2_plain(double& a, double& b, const double* p) {
+  asm volatile("ld.global.cs.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "l"(p));
+}
+
 // Where the group's next P rows come from when they can be fetched with aligned 128-bit loads.
 struct NextChunk {
   const double* base;   // x.base + r_next + 2*grp (row pair of this group in the next chunk)
@@ -77,13 +84,19 @@ struct Fold {
   static constexpr int NPAD = NS * G;
   static constexpr int GW = 32 / G;
 
-  template <int S>
+  // FULL: the caller knows that the next chunk is a full, aligned one (only used with G == 1)
+  template <int S, bool FULL = false>
   static __device__ __forceinline__ void refill(double (&w)[NS][P], const NextChunk& nx, int g) {
     const int col = S * G + g;
     const double* cp = col < nx.n_main ? nx.base + static_cast<long long>(col) * nx.ld : nx.extra;
-    const int pred = nx.pred && col < nx.n;
+    if constexpr (FULL && G == 1) {
 #pragma unroll
-    for (int k = 0; k < P / 2; ++k) ld2_pred(w[S][2 * k], w[S][2 * k + 1], cp + 2 * GW * k, pred);
+      for (int k = 0; k < P / 2; ++k) ld2_plain(w[S][2 * k], w[S][2 * k + 1], cp + 2 * GW * k);
+    } else {
+      const int pred = nx.pred && col < nx.n;
+#pragma unroll
+      for (int k = 0; k < P / 2; ++k) ld2_pred(w[S][2 * k], w[S][2 * k + 1], cp + 2 * GW * k, pred);
+    }
   }
 
   // column `S`-slot, lane `src` of the group -> v on every lane, plus its reflector
@@ -109,7 +122,7 @@ struct Fold {
   // GUARD: the triangle is only written when `store` (merge tree: a group without a partner folds zero rows
   // beside the others because the shuffles are warp-wide; its triangle is being read by its own partner's
   // owner at a lower slot, so it must not be written, not even with unchanged values).
-  template <int BC, bool PEEL, bool GUARD>
+  template <int BC, bool PEEL, bool GUARD, bool FULL = false>
   static __device__ __forceinline__ void step(double (&w)[NS][P], double (&v)[P], Reflector& h,
                                               double* tri, int& rowoff, int g, int gc,
                                               const NextChunk& nx, bool store) {
@@ -160,7 +173,7 @@ struct Fold {
       });
     }
     if ((!GUARD || store) && g == gc) tri[rowoff + c] = h.beta;
-    if constexpr (PEEL && BC < NS - 1) refill<BC>(w, nx, g);
+    if constexpr (PEEL && BC < NS - 1) refill<BC, FULL>(w, nx, g);
     if constexpr (HAS_NEXT) {
       if constexpr (G > 1) {
 #pragma unroll
@@ -176,7 +189,7 @@ struct Fold {
 
   // Fold the group's P x n register panel into its triangle; on return the panel holds the rows
   // named by `nx` (or zeros).
-  template <bool GUARD = false>
+  template <bool GUARD = false, bool FULL = false>
   static __device__ __forceinline__ void run(double (&w)[NS][P], double* tri, int n, int g,
                                              const NextChunk& nx, bool store = true) {
     double v[P];
@@ -189,18 +202,18 @@ struct Fold {
       if constexpr (bc < NS - 1) {
         if constexpr (G > 1) {
 #pragma unroll 1
-          for (int gc = 0; gc < G - 1; ++gc) step<bc, false, GUARD>(w, v, h, tri, rowoff, g, gc, nx, store);
+          for (int gc = 0; gc < G - 1; ++gc) step<bc, false, GUARD, FULL>(w, v, h, tri, rowoff, g, gc, nx, store);
         }
-        step<bc, true, GUARD>(w, v, h, tri, rowoff, g, G - 1, nx, store);
+        step<bc, true, GUARD, FULL>(w, v, h, tri, rowoff, g, G - 1, nx, store);
       } else {
         const int cols_last = n - bc * G;  // 1..G live columns in the last slot
         if constexpr (G > 1) {
           const int lim = cols_last < G - 1 ? cols_last : G - 1;
 #pragma unroll 1
-          for (int gc = 0; gc < lim; ++gc) step<bc, false, GUARD>(w, v, h, tri, rowoff, g, gc, nx, store);
+          for (int gc = 0; gc < lim; ++gc) step<bc, false, GUARD, FULL>(w, v, h, tri, rowoff, g, gc, nx, store);
         }
-        if (cols_last == G) step<bc, true, GUARD>(w, v, h, tri, rowoff, g, G - 1, nx, store);
-        refill<bc>(w, nx, g);
+        if (cols_last == G) step<bc, true, GUARD, FULL>(w, v, h, tri, rowoff, g, G - 1, nx, store);
+        refill<bc, FULL>(w, nx, g);
       }
     });
   }
@@ -261,7 +274,12 @@ __global__ void __launch_bounds__(FoldCfg<NS, G, P, TMAX>::T, 1) tsqr_fold_kerne
     nx.base = prm.x.base + rn + 2 * grp;
     nx.extra = prm.x.extra + rn + 2 * grp;
     nx.pred = fast ? 1 : 0;
-    Fold<NS, G, P>::run(w, tri, n, g, nx);
+    if constexpr (G == 1) {  // n == NS here: a full next chunk needs neither predicates nor zero fill
+      if (fast) Fold<NS, G, P>::template run<false, true>(w, tri, n, g, nx);
+      else Fold<NS, G, P>::run(w, tri, n, g, nx);
+    } else {
+      Fold<NS, G, P>::run(w, tri, n, g, nx);
+    }
     loaded = fast;
   }
 
