@@ -84,12 +84,12 @@ struct Fold {
   static constexpr int NPAD = NS * G;
   static constexpr int GW = 32 / G;
 
-  // FULL: the caller knows that the next chunk is a full, aligned one (only used with G == 1)
+  // FULL: the caller knows that the next chunk is a full, aligned one
   template <int S, bool FULL = false>
   static __device__ __forceinline__ void refill(double (&w)[NS][P], const NextChunk& nx, int g) {
     const int col = S * G + g;
     const double* cp = col < nx.n_main ? nx.base + static_cast<long long>(col) * nx.ld : nx.extra;
-    if constexpr (FULL && G == 1) {
+    if constexpr (FULL && (G == 1 || S < NS - 1)) {  // every slot but the last holds live columns only (n > (NS-1) G)
 #pragma unroll
       for (int k = 0; k < P / 2; ++k) ld2_plain(w[S][2 * k], w[S][2 * k + 1], cp + 2 * GW * k);
     } else {
@@ -274,7 +274,11 @@ __global__ void __launch_bounds__(FoldCfg<NS, G, P, TMAX>::T, 1) tsqr_fold_kerne
     nx.base = prm.x.base + rn + 2 * grp;
     nx.extra = prm.x.extra + rn + 2 * grp;
     nx.pred = fast ? 1 : 0;
-    if constexpr (G == 1) {  // n == NS here: a full next chunk needs neither predicates nor zero fill
+    // a full next chunk needs neither predicates nor zero fill (G > 1: except in the last, possibly padded slot).
+    // Measured per group size (profiles/probes/r02_tsqr_experiments.txt, 8): +3-4 % for thread-private leaves from
+    // 9 columns on and for lane quads, -3..-11 % for lane pairs (the second copy of the fold pushes ptxas into a
+    // worse schedule there), so pairs keep the single predicated path
+    if constexpr (G == 1 || G == 4) {
       if (fast) Fold<NS, G, P>::template run<false, true>(w, tri, n, g, nx);
       else Fold<NS, G, P>::run(w, tri, n, g, nx);
     } else {
